@@ -1,0 +1,1006 @@
+// gtcp_api.cu -- host orchestration behind the C ABI of include/gtcp.h.
+//
+// One context per rank (one process per GPU).  All device work is enqueued on
+// the context stream; NCCL runs on the same stream, so ordering is implicit.
+// Geometry (G-1..G-4) is rebuilt here on the host from the paper's rules
+// (product-side code; the oracle has its own independent implementation).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gtcp_internal.cuh"
+
+using namespace gtcp;
+
+struct gtcp_ctx_s {
+    gtcp_params prm;
+    int rank, nranks, rank_t, rank_p;
+    cudaStream_t st;
+    int device;
+    ncclComm_t world = nullptr, tor = nullptr, part = nullptr;
+    std::string err;
+    gtcp_status sticky = GTCP_OK;
+    // geometry (host + device)
+    std::vector<int> mtheta, igrid, itran;
+    std::vector<double> qtinv;
+    int mgrid = 0, P = 0, k0 = 0;
+    int *d_mtheta = nullptr, *d_igrid = nullptr, *d_itran = nullptr;
+    double* d_qtinv = nullptr;
+    Geo geo;
+    // particles
+    long long n = 0, cap = 0;
+    double* bufA[5] = {};
+    double* bufB[5] = {};
+    double* live[5] = {};
+    double* saved[5] = {};
+    double* mu = nullptr;
+    double* scratch = nullptr;
+    unsigned long long* id = nullptr;
+    unsigned long long* id_scratch = nullptr;
+    int stage_next = 1;
+    int steps_done = 0;
+    // binning
+    long long nkeys = 0;
+    unsigned *key = nullptr, *rankbuf = nullptr, *count = nullptr, *offset = nullptr, *scan_tmp = nullptr;
+    Tile* tiles = nullptr;
+    int max_tiles = 0;
+    long long n_binned = 0;  // particles [0, n_binned) are covered by tiles
+    int tile_max = 8192;
+    // grids
+    long long* fx = nullptr;   // (P+1) * mgrid fixed-point charge
+    double *rhoH = nullptr, *dnH = nullptr, *tmpH = nullptr, *phiH = nullptr;
+    double *rhs = nullptr, *jphi = nullptr, *g1 = nullptr, *g2 = nullptr;
+    double* gfield = nullptr;  // P * mgrid * 6
+    double* nm = nullptr;      // mpsi+1 marker density
+    double* ringsum = nullptr; // mpsi+1
+    double* phi00 = nullptr;   // 5 * (mpsi+1)
+    double* halo_buf = nullptr;  // 3 * mgrid receive buffer
+    long long* fx_recv = nullptr;  // mgrid
+    DevCounters* dc = nullptr;
+    DevCounters* h_dc = nullptr;  // pinned host mirror
+    double* d_scalar = nullptr;   // small device scratch (sums)
+    double* d_partial = nullptr;  // 1024 partial sums
+    double* h_scalar = nullptr;   // pinned
+    // shift buffers
+    long long shift_cap = 0;
+    double* sendL[12] = {};
+    double* sendR[12] = {};
+    double* recvL[12] = {};
+    double* recvR[12] = {};
+    unsigned long long *sidL = nullptr, *sidR = nullptr, *ridL = nullptr, *ridR = nullptr;
+    unsigned char* cls = nullptr;
+    unsigned* bcount = nullptr;  // per-block counts (3 per block) + scan
+    int shift_blocks = 0;
+    long long movers_sent = 0, movers_recv = 0;
+    // charge config
+    int charge_mode = 0;
+    int dep_ctas = 0, dep_cap_nodes = 0;
+    size_t dep_smem = 0;
+    // timing
+    bool timing = false;
+    struct Pending { int phase; cudaEvent_t a, b; };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> event_pool;
+    double t_ms[GTCP_NPHASE] = {};
+    long long t_calls[GTCP_NPHASE] = {};
+    long long launches0 = 0;
+};
+
+// ----------------------------------------------------------------------------
+// error helpers
+// ----------------------------------------------------------------------------
+static gtcp_status set_err(gtcp_ctx c, gtcp_status s, const std::string& msg) {
+    if (c) {
+        c->err = msg;
+        if (s == GTCP_ECUDA || s == GTCP_ENCCL) c->sticky = s;
+    }
+    return s;
+}
+
+#define CU(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t _e = (call);                                                                   \
+        if (_e != cudaSuccess)                                                                     \
+            return set_err(c, GTCP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e));     \
+    } while (0)
+#define NC(call)                                                                                   \
+    do {                                                                                           \
+        ncclResult_t _r = (call);                                                                  \
+        if (_r != ncclSuccess)                                                                     \
+            return set_err(c, GTCP_ENCCL, std::string(#call) + ": " + ncclGetErrorString(_r));     \
+    } while (0)
+#define CHECK_CTX(c)                                                                               \
+    do {                                                                                           \
+        if (!(c)) return GTCP_EINVAL;                                                              \
+        if ((c)->sticky != GTCP_OK) return GTCP_ESTATE;                                            \
+    } while (0)
+#define KCHECK()                                                                                   \
+    do {                                                                                           \
+        cudaError_t _e = cudaGetLastError();                                                       \
+        if (_e != cudaSuccess) return set_err(c, GTCP_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+    } while (0)
+
+// ----------------------------------------------------------------------------
+// timing (CUDA events on the context stream)
+// ----------------------------------------------------------------------------
+static cudaEvent_t get_event(gtcp_ctx c) {
+    if (!c->event_pool.empty()) {
+        cudaEvent_t e = c->event_pool.back();
+        c->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+static void fold_pending(gtcp_ctx c) {
+    for (auto& p : c->pending) {
+        cudaEventSynchronize(p.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, p.a, p.b);
+        c->t_ms[p.phase] += ms;
+        c->t_calls[p.phase]++;
+        c->event_pool.push_back(p.a);
+        c->event_pool.push_back(p.b);
+    }
+    c->pending.clear();
+}
+
+struct PhaseTimer {
+    gtcp_ctx c;
+    int phase;
+    cudaEvent_t a = nullptr;
+    PhaseTimer(gtcp_ctx c_, int ph) : c(c_), phase(ph) {
+        if (c->timing) {
+            a = get_event(c);
+            cudaEventRecord(a, c->st);
+        }
+    }
+    ~PhaseTimer() {
+        if (c->timing) {
+            cudaEvent_t b = get_event(c);
+            cudaEventRecord(b, c->st);
+            c->pending.push_back({phase, a, b});
+            if (c->pending.size() > 4096) fold_pending(c);
+        }
+    }
+};
+
+// ----------------------------------------------------------------------------
+// geometry (G-1..G-4; Tab.2) -- product-side host implementation
+// ----------------------------------------------------------------------------
+static long long build_geometry(const gtcp_params* p, std::vector<int>& mtheta, std::vector<int>& igrid,
+                                std::vector<int>& itran, std::vector<double>& qtinv) {
+    int M = p->mpsi;
+    mtheta.assign(M + 1, 0);
+    igrid.assign(M + 2, 0);
+    itran.assign(M + 1, 0);
+    qtinv.assign(M + 1, 0.0);
+    double dr = (p->a1 - p->a0) / M;
+    long long acc = 0;
+    for (int i = 0; i <= M; i++) {
+        double r = p->a0 + i * dr;
+        int mt = 2 * (int)std::floor(p->mthetamax * r / (2.0 * p->a1) + 0.5);
+        double q = p->q0 + p->q2 * r * r;
+        mtheta[i] = mt;
+        itran[i] = (int)std::floor(mt / q + 0.5);
+        qtinv[i] = (double)itran[i] / (double)mt;
+        igrid[i] = (int)acc;
+        acc += mt + 1;
+    }
+    igrid[M + 1] = (int)acc;
+    return acc;
+}
+
+extern "C" gtcp_status gtcp_default_params(char size, gtcp_params* out) {
+    if (!out) return GTCP_EINVAL;
+    int mpsi, mth, mze = 64, micell = 100;
+    switch (size) {
+        case 'T': mpsi = 16; mth = 64; mze = 2; micell = 10; break;
+        case 'A': case 'a': mpsi = 90; mth = 640; break;
+        case 'B': mpsi = 192; mth = 1408; break;
+        case 'C': mpsi = 384; mth = 2816; break;
+        case 'D': mpsi = 768; mth = 5632; break;
+        case 'b': mpsi = 180; mth = 1280; break;
+        case 'c': mpsi = 360; mth = 2560; break;
+        case 'd': mpsi = 720; mth = 5120; break;
+        default: return GTCP_EINVAL;
+    }
+    gtcp_params p;
+    memset(&p, 0, sizeof(p));
+    p.mpsi = mpsi; p.mthetamax = mth; p.mzetamax = mze; p.micell = micell;
+    p.ntoroidal = 1; p.npartdom = 1;
+    p.precision = 64; p.bin_every = 10; p.poisson_iters = 20; p.paranl = 1; p.drifts = 1; p.track_ids = 0;
+    p.a0 = 0.1; p.a1 = 0.9; p.R0 = 2.78; p.omega0 = 125.0 * mpsi / 90.0;
+    p.q0 = 0.854; p.q2 = 2.184; p.rln = 2.2; p.rlt = 6.9; p.tau = 1.0; p.dt = 0.06;
+    p.jacobi_omega = 1.0; p.w_init_amp = 1e-3; p.vcut = 5.0; p.capacity_factor = 1.0;
+    p.seed = 2;
+    *out = p;
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_geometry(const gtcp_params* p, int32_t* mtheta, int64_t* igrid, int32_t* itran,
+                                     double* qtinv, int64_t* mgrid) {
+    if (!p || p->mpsi < 2 || p->mthetamax < 4) return GTCP_EINVAL;
+    std::vector<int> mt, ig, it;
+    std::vector<double> qt;
+    long long mg = build_geometry(p, mt, ig, it, qt);
+    for (int i = 0; i <= p->mpsi; i++) {
+        if (mtheta) mtheta[i] = mt[i];
+        if (itran) itran[i] = it[i];
+        if (qtinv) qtinv[i] = qt[i];
+    }
+    if (igrid)
+        for (int i = 0; i <= p->mpsi + 1; i++) igrid[i] = ig[i];
+    if (mgrid) *mgrid = mg;
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_nccl_unique_id(void* out128) {
+    if (!out128) return GTCP_EINVAL;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return GTCP_ENCCL;
+    memcpy(out128, &id, sizeof(id));
+    return GTCP_OK;
+}
+
+// ----------------------------------------------------------------------------
+// init / destroy
+// ----------------------------------------------------------------------------
+template <class T>
+static cudaError_t dalloc(T** p, size_t count) {
+    return cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T));
+}
+
+extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, const void* nccl_id,
+                                 void* cuda_stream, gtcp_ctx* out) {
+    if (!p || !out || nranks < 1 || rank < 0 || rank >= nranks) return GTCP_EINVAL;
+    if (p->precision != 64) return GTCP_EINVAL;
+    if (p->mpsi < 2 || p->mthetamax < 4 || p->mzetamax < 2 || p->micell < 0) return GTCP_EINVAL;
+    if (p->ntoroidal < 1 || p->npartdom < 1) return GTCP_EINVAL;
+    if (p->mzetamax % p->ntoroidal != 0 || p->ntoroidal * p->npartdom != nranks) return GTCP_EINVARIANT;
+    if (p->mzetamax / p->ntoroidal < 2) return GTCP_EINVARIANT;
+    if (nranks > 1 && !nccl_id) return GTCP_EINVAL;
+    gtcp_ctx c = new gtcp_ctx_s();
+    c->prm = *p;
+    c->rank = rank;
+    c->nranks = nranks;
+    c->rank_t = rank / p->npartdom;
+    c->rank_p = rank % p->npartdom;
+    c->st = (cudaStream_t)cuda_stream;
+    cudaGetDevice(&c->device);
+    *out = c;
+    c->mgrid = (int)build_geometry(p, c->mtheta, c->igrid, c->itran, c->qtinv);
+    c->P = p->mzetamax / p->ntoroidal;
+    c->k0 = c->rank_t * c->P;
+    const int M = p->mpsi, mg = c->mgrid, P = c->P;
+    CU(dalloc(&c->d_mtheta, M + 1));
+    CU(dalloc(&c->d_igrid, M + 2));
+    CU(dalloc(&c->d_itran, M + 1));
+    CU(dalloc(&c->d_qtinv, M + 1));
+    CU(cudaMemcpy(c->d_mtheta, c->mtheta.data(), sizeof(int) * (M + 1), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(c->d_igrid, c->igrid.data(), sizeof(int) * (M + 2), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(c->d_itran, c->itran.data(), sizeof(int) * (M + 1), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(c->d_qtinv, c->qtinv.data(), sizeof(double) * (M + 1), cudaMemcpyHostToDevice));
+    Geo& g = c->geo;
+    g.mpsi = M; g.mzetamax = p->mzetamax; g.P = P; g.k0 = c->k0; g.ntor = p->ntoroidal; g.rank_t = c->rank_t;
+    g.mgrid = mg; g.paranl = p->paranl; g.drifts = p->drifts;
+    g.a0 = p->a0; g.a1 = p->a1; g.dr = (p->a1 - p->a0) / M; g.inv_dr = 1.0 / g.dr;
+    g.R0 = p->R0; g.inv_R0 = 1.0 / p->R0; g.omega0 = p->omega0; g.q0 = p->q0; g.q2 = p->q2;
+    g.rln = p->rln; g.rlt = p->rlt; g.tau = p->tau; g.dt = p->dt;
+    g.cz = p->mzetamax / GTCP_TWO_PI;
+    g.dzeta = GTCP_TWO_PI / p->mzetamax;
+    g.rhoG = std::sqrt(2.0) / p->omega0;
+    g.mtheta = c->d_mtheta; g.igrid = c->d_igrid; g.itran = c->d_itran; g.qtinv = c->d_qtinv;
+    // particle capacity: the loaded count plus headroom for shift imbalance
+    long long per_plane = (long long)p->micell * (mg - M);
+    long long n_load = per_plane * P / p->npartdom;
+    double headroom = nranks > 1 ? 0.10 : 0.0;
+    c->cap = (long long)std::ceil(n_load * (p->capacity_factor + headroom)) + 1024;
+    for (int d = 0; d < 5; d++) {
+        CU(dalloc(&c->bufA[d], c->cap));
+        CU(dalloc(&c->bufB[d], c->cap));
+        c->live[d] = c->bufA[d];
+        c->saved[d] = c->bufB[d];
+    }
+    CU(dalloc(&c->mu, c->cap));
+    CU(dalloc(&c->scratch, c->cap));
+    if (p->track_ids) {
+        CU(dalloc(&c->id, c->cap));
+        CU(dalloc(&c->id_scratch, c->cap));
+    }
+    // binning
+    c->nkeys = (long long)mg * P;
+    CU(dalloc(&c->key, c->cap));
+    CU(dalloc(&c->rankbuf, c->cap));
+    CU(dalloc(&c->count, c->nkeys + 1));
+    CU(dalloc(&c->offset, c->nkeys + 1));
+    CU(dalloc(&c->scan_tmp, (c->nkeys + 4095) / 4096 + 1));
+    c->max_tiles = (int)std::min<long long>((long long)mg + c->cap / 1024 + M + 16, 1LL << 30);
+    CU(dalloc(&c->tiles, c->max_tiles));
+    // grids
+    long long HP = (long long)(P + 3) * mg;
+    CU(dalloc(&c->fx, (long long)(P + 1) * mg));
+    CU(dalloc(&c->rhoH, HP));
+    CU(dalloc(&c->dnH, HP));
+    CU(dalloc(&c->tmpH, HP));
+    CU(dalloc(&c->phiH, HP));
+    CU(cudaMemset(c->rhoH, 0, HP * sizeof(double)));
+    CU(cudaMemset(c->dnH, 0, HP * sizeof(double)));
+    CU(cudaMemset(c->tmpH, 0, HP * sizeof(double)));
+    CU(cudaMemset(c->phiH, 0, HP * sizeof(double)));
+    CU(dalloc(&c->rhs, (long long)P * mg));
+    CU(dalloc(&c->jphi, (long long)P * mg));
+    CU(dalloc(&c->g1, (long long)P * mg));
+    CU(dalloc(&c->g2, (long long)P * mg));
+    CU(dalloc(&c->gfield, (long long)P * mg * 6));
+    CU(cudaMemset(c->gfield, 0, (long long)P * mg * 6 * sizeof(double)));
+    CU(dalloc(&c->nm, M + 1));
+    CU(dalloc(&c->ringsum, M + 1));
+    CU(dalloc(&c->phi00, 5 * (M + 1)));
+    CU(dalloc(&c->halo_buf, 3LL * mg));
+    CU(dalloc(&c->fx_recv, mg));
+    CU(dalloc(&c->dc, 1));
+    CU(cudaMemset(c->dc, 0, sizeof(DevCounters)));
+    CU(cudaMallocHost((void**)&c->h_dc, sizeof(DevCounters)));
+    CU(dalloc(&c->d_scalar, 16));
+    CU(dalloc(&c->d_partial, 1024));
+    CU(cudaMallocHost((void**)&c->h_scalar, 16 * sizeof(double)));
+    {
+        std::vector<double> ones(M + 1, 1.0);
+        CU(cudaMemcpy(c->nm, ones.data(), sizeof(double) * (M + 1), cudaMemcpyHostToDevice));
+    }
+    // tiled deposit launch configuration: 2 CTAs of 512 threads per SM
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+    int smem_optin = 0;
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+    size_t table_bytes = (size_t)(P + 1) * 16 * sizeof(int);
+    size_t per_cta = std::min<size_t>((size_t)smem_optin, 110 * 1024);
+    if (per_cta < table_bytes + 8 * 1024) {
+        c->dep_cap_nodes = 0;
+    } else {
+        c->dep_cap_nodes = (int)((per_cta - table_bytes - 1024) / 8);
+    }
+    c->dep_smem = (size_t)c->dep_cap_nodes * 8 + table_bytes;
+    c->dep_ctas = nsm * 2;
+    if (P + 1 > 80 || c->dep_cap_nodes < 1024) c->charge_mode = 1;
+    else CU(configure_deposit_tiled(c->dep_smem));
+    c->launches0 = gtcp::g_launches;
+    // NCCL communicators
+    if (nranks > 1) {
+        ncclUniqueId uid;
+        memcpy(&uid, nccl_id, sizeof(uid));
+        NC(ncclCommInitRank(&c->world, nranks, uid, rank));
+        NC(ncclCommSplit(c->world, c->rank_p, c->rank_t, &c->tor, nullptr));
+        NC(ncclCommSplit(c->world, c->rank_t, c->rank_p, &c->part, nullptr));
+    }
+    // shift buffers (movers per stage ~1% at 8 domains; allocate generously)
+    if (p->ntoroidal > 1) {
+        c->shift_cap = std::max<long long>(1 << 16, (long long)(0.08 * c->cap));
+        for (int d = 0; d < 11; d++) {
+            CU(dalloc(&c->sendL[d], c->shift_cap));
+            CU(dalloc(&c->sendR[d], c->shift_cap));
+            CU(dalloc(&c->recvL[d], c->shift_cap));
+            CU(dalloc(&c->recvR[d], c->shift_cap));
+        }
+        if (p->track_ids) {
+            CU(dalloc(&c->sidL, c->shift_cap));
+            CU(dalloc(&c->sidR, c->shift_cap));
+            CU(dalloc(&c->ridL, c->shift_cap));
+            CU(dalloc(&c->ridR, c->shift_cap));
+        }
+        CU(dalloc(&c->cls, c->cap));
+        c->shift_blocks = (int)((c->cap + 1023) / 1024);
+        CU(dalloc(&c->bcount, 3LL * (c->shift_blocks + 1) * 2));
+    }
+    CU(cudaDeviceSynchronize());
+    return GTCP_OK;
+}
+
+extern "C" void gtcp_destroy(gtcp_ctx c) {
+    if (!c) return;
+    cudaStreamSynchronize(c->st);
+    fold_pending(c);
+    for (auto e : c->event_pool) cudaEventDestroy(e);
+    auto F = [](void* p) { if (p) cudaFree(p); };
+    for (int d = 0; d < 5; d++) { F(c->bufA[d]); F(c->bufB[d]); }
+    F(c->mu); F(c->scratch); F(c->id); F(c->id_scratch);
+    F(c->key); F(c->rankbuf); F(c->count); F(c->offset); F(c->scan_tmp); F(c->tiles);
+    F(c->fx); F(c->rhoH); F(c->dnH); F(c->tmpH); F(c->phiH); F(c->rhs); F(c->jphi); F(c->g1); F(c->g2);
+    F(c->gfield); F(c->nm); F(c->ringsum); F(c->phi00); F(c->halo_buf); F(c->fx_recv); F(c->dc); F(c->d_scalar); F(c->d_partial);
+    F(c->d_mtheta); F(c->d_igrid); F(c->d_itran); F(c->d_qtinv);
+    for (int d = 0; d < 12; d++) { F(c->sendL[d]); F(c->sendR[d]); F(c->recvL[d]); F(c->recvR[d]); }
+    F(c->sidL); F(c->sidR); F(c->ridL); F(c->ridR); F(c->cls); F(c->bcount);
+    if (c->h_dc) cudaFreeHost(c->h_dc);
+    if (c->h_scalar) cudaFreeHost(c->h_scalar);
+    if (c->part) ncclCommDestroy(c->part);
+    if (c->tor) ncclCommDestroy(c->tor);
+    if (c->world) ncclCommDestroy(c->world);
+    delete c;
+}
+
+extern "C" const char* gtcp_strerror(gtcp_ctx c) { return c ? c->err.c_str() : "null context"; }
+
+extern "C" gtcp_status gtcp_info(gtcp_ctx c, gtcp_info_t* out) {
+    if (!c || !out) return GTCP_EINVAL;
+    out->mgrid = c->mgrid;
+    out->P = c->P;
+    out->k0 = c->k0;
+    out->rank_toroidal = c->rank_t;
+    out->rank_particle = c->rank_p;
+    out->n_local = c->n;
+    out->capacity = c->cap;
+    out->stage_next = c->stage_next;
+    out->steps_done = c->steps_done;
+    return GTCP_OK;
+}
+
+static PSet live_set(gtcp_ctx c) {
+    PSet s;
+    for (int d = 0; d < 5; d++) { s.x[d] = c->live[d]; s.x0[d] = c->saved[d]; }
+    s.mu = c->mu;
+    s.id = c->id;
+    return s;
+}
+
+// ----------------------------------------------------------------------------
+// halo exchange of an H array (planes -1..P+1): plane -1 <- left neighbour's
+// P-1; planes P, P+1 <- right neighbour's 0, 1; seam rotation at zeta = 2 pi.
+// ----------------------------------------------------------------------------
+static gtcp_status halo_exchange(gtcp_ctx c, double* H) {
+    const Geo& g = c->geo;
+    const long long mg = c->mgrid;
+    const int P = c->P;
+    double* pm1 = H;                       // plane -1
+    double* p0 = H + mg;                   // plane 0
+    double* pP = H + (long long)(P + 1) * mg;
+    if (c->prm.ntoroidal == 1) {
+        launch_seam_rotate(g, H + (long long)P * mg, pm1, -1, c->st);       // plane P-1 -> -1
+        launch_seam_rotate(g, p0, pP, +1, c->st);                            // plane 0 -> P
+        launch_seam_rotate(g, p0 + mg, pP + mg, +1, c->st);                  // plane 1 -> P+1
+        KCHECK();
+        return GTCP_OK;
+    }
+    int nt = c->prm.ntoroidal;
+    int left = (c->rank_t - 1 + nt) % nt, right = (c->rank_t + 1) % nt;
+    double* rb = c->halo_buf;  // [0]: from left (their P-1), [1..2]: from right (their 0, 1)
+    NC(ncclGroupStart());
+    NC(ncclSend(p0, 2 * mg, ncclDouble, left, c->tor, c->st));
+    NC(ncclSend(H + (long long)P * mg, mg, ncclDouble, right, c->tor, c->st));
+    NC(ncclRecv(rb, mg, ncclDouble, left, c->tor, c->st));
+    NC(ncclRecv(rb + mg, 2 * mg, ncclDouble, right, c->tor, c->st));
+    NC(ncclGroupEnd());
+    if (c->rank_t == 0) launch_seam_rotate(g, rb, pm1, -1, c->st);
+    else CU(cudaMemcpyAsync(pm1, rb, mg * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    if (c->rank_t == nt - 1) {
+        launch_seam_rotate(g, rb + mg, pP, +1, c->st);
+        launch_seam_rotate(g, rb + 2 * mg, pP + mg, +1, c->st);
+    } else {
+        CU(cudaMemcpyAsync(pP, rb + mg, 2 * mg * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    }
+    KCHECK();
+    return GTCP_OK;
+}
+
+// ----------------------------------------------------------------------------
+// charge
+// ----------------------------------------------------------------------------
+static bool g_unit_weight = false;  // marker-density deposit (w == 1)
+
+static gtcp_status deposit_fx(gtcp_ctx c) {
+    const Geo& g = c->geo;
+    PSet s = live_set(c);
+    if (g_unit_weight) {
+        // w == 1: point the weight array at a constant-one buffer (scratch)
+        s.x[4] = c->scratch;
+    }
+    launch_fx_scale(c->dc, c->st);
+    CU(cudaMemsetAsync(c->fx, 0, (size_t)(c->P + 1) * c->mgrid * sizeof(long long), c->st));
+    long long tiled_end = 0;
+    if (c->charge_mode == 0 && c->n_binned > 0) {
+        launch_deposit_tiled(g, s, std::min(c->n, c->n_binned), c->tiles, c->max_tiles, c->fx, c->dc, c->dep_ctas,
+                             c->dep_smem, c->dep_cap_nodes, c->st);
+        tiled_end = std::min(c->n, c->n_binned);
+    }
+    launch_deposit_direct(g, s, tiled_end, c->n, c->fx, c->dc, c->st);
+    KCHECK();
+    return GTCP_OK;
+}
+
+// Q-7 reductions on the fixed-point grid, then fp64 rho (H array, planes 0..P
+// plus halos).
+static gtcp_status charge_reduce(gtcp_ctx c) {
+    const Geo& g = c->geo;
+    const long long mg = c->mgrid;
+    const int P = c->P;
+    if (c->prm.ntoroidal > 1) {
+        int nt = c->prm.ntoroidal;
+        int left = (c->rank_t - 1 + nt) % nt, right = (c->rank_t + 1) % nt;
+        NC(ncclGroupStart());
+        NC(ncclSend(c->fx + (long long)P * mg, mg, ncclInt64, right, c->tor, c->st));
+        NC(ncclRecv(c->fx_recv, mg, ncclInt64, left, c->tor, c->st));
+        NC(ncclGroupEnd());
+        launch_rotate_add_i64(g, c->fx_recv, c->fx, c->rank_t == 0 ? +1 : 0, c->st);
+    }
+    if (c->prm.npartdom > 1) {
+        NC(ncclAllReduce(c->fx, c->fx, (size_t)P * mg, ncclInt64, ncclSum, c->part, c->st));
+    }
+    launch_fx_to_real(g, c->fx, c->rhoH + mg, c->dc, P, c->st);
+    launch_fill_dup(g, c->rhoH + mg, P, 1, c->st);
+    KCHECK();
+    return halo_exchange(c, c->rhoH);
+}
+
+static gtcp_status compute_marker_norm(gtcp_ctx c) {
+    // deposit with w == 1 (Q-8): scratch := 1, wmax := 1
+    const Geo& g = c->geo;
+    {
+        double v1 = 1.0;
+        memcpy(&c->h_scalar[8], &v1, 8);
+        CU(cudaMemcpyAsync(&c->dc->wmax_bits, &c->h_scalar[8], 8, cudaMemcpyHostToDevice, c->st));
+        launch_fill_f64(c->scratch, c->n, 1.0, c->st);
+    }
+    g_unit_weight = true;
+    gtcp_status s = deposit_fx(c);
+    g_unit_weight = false;
+    if (s != GTCP_OK) return s;
+    s = charge_reduce(c);
+    if (s != GTCP_OK) return s;
+    launch_ring_sum(g, c->rhoH, c->ringsum, c->st);
+    if (c->prm.ntoroidal > 1) NC(ncclAllReduce(c->ringsum, c->ringsum, g.mpsi + 1, ncclDouble, ncclSum, c->tor, c->st));
+    launch_ring_mean(g, c->ringsum, c->nm, c->st);
+    // restore max|w| of the real weights
+    CU(cudaMemsetAsync(&c->dc->wmax_bits, 0, 8, c->st));
+    launch_wmax(c->live[4], c->n, c->dc, c->st);
+    KCHECK();
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_charge(gtcp_ctx c) {
+    CHECK_CTX(c);
+    {
+        PhaseTimer t(c, GTCP_T_CHARGE);
+        gtcp_status s = deposit_fx(c);
+        if (s != GTCP_OK) return s;
+    }
+    PhaseTimer t(c, GTCP_T_CHARGE_RED);
+    return charge_reduce(c);
+}
+
+// ----------------------------------------------------------------------------
+// poisson_smooth / field
+// ----------------------------------------------------------------------------
+// F-4 smooth of H array `f` (owned planes), result back in `f`; uses tmpH.
+static gtcp_status smooth_H(gtcp_ctx c, double* f) {
+    const Geo& g = c->geo;
+    launch_smooth_theta(g, f, c->tmpH, c->st);
+    launch_smooth_r(g, c->tmpH, f, c->st);
+    KCHECK();
+    gtcp_status s = halo_exchange(c, f);
+    if (s != GTCP_OK) return s;
+    launch_smooth_par(g, f, c->tmpH, c->st);
+    CU(cudaMemcpyAsync(f + c->mgrid, c->tmpH + c->mgrid, (size_t)c->P * c->mgrid * sizeof(double),
+                       cudaMemcpyDeviceToDevice, c->st));
+    KCHECK();
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_poisson_smooth(gtcp_ctx c) {
+    CHECK_CTX(c);
+    PhaseTimer t(c, GTCP_T_POISSON);
+    const Geo& g = c->geo;
+    launch_normalize(g, c->rhoH + c->mgrid, c->nm, c->dnH, c->st);
+    gtcp_status s = smooth_H(c, c->dnH);
+    if (s != GTCP_OK) return s;
+    launch_ring_sum(g, c->dnH, c->ringsum, c->st);
+    if (c->prm.ntoroidal > 1) NC(ncclAllReduce(c->ringsum, c->ringsum, g.mpsi + 1, ncclDouble, ncclSum, c->tor, c->st));
+    launch_jacobi_init(g, c->dnH, c->ringsum, c->rhs, c->jphi, c->st);
+    for (int it = 0; it < c->prm.poisson_iters; it++) {
+        launch_gyro(g, c->jphi, c->g1, c->st);
+        launch_gyro(g, c->g1, c->g2, c->st);
+        launch_jacobi_update(g, c->rhs, c->g2, c->jphi, c->prm.jacobi_omega, c->st);
+    }
+    launch_zonal(g, c->ringsum, c->phi00, c->st);
+    launch_add_zonal2(g, c->phi00, c->jphi, c->phiH, c->st);
+    launch_fill_dup(g, c->phiH + c->mgrid, c->P, 1, c->st);
+    KCHECK();
+    s = halo_exchange(c, c->phiH);
+    if (s != GTCP_OK) return s;
+    s = smooth_H(c, c->phiH);
+    if (s != GTCP_OK) return s;
+    return halo_exchange(c, c->phiH);
+}
+
+extern "C" gtcp_status gtcp_field(gtcp_ctx c) {
+    CHECK_CTX(c);
+    PhaseTimer t(c, GTCP_T_FIELD);
+    launch_field(c->geo, c->phiH, c->gfield, c->st);
+    KCHECK();
+    return GTCP_OK;
+}
+
+// ----------------------------------------------------------------------------
+// push
+// ----------------------------------------------------------------------------
+extern "C" gtcp_status gtcp_push(gtcp_ctx c, int stage) {
+    CHECK_CTX(c);
+    if (stage != c->stage_next) return set_err(c, GTCP_ESTATE, "push: unexpected RK2 stage");
+    PhaseTimer t(c, GTCP_T_PUSH);
+    CU(cudaMemsetAsync(&c->dc->wmax_bits, 0, 8, c->st));
+    if (stage == 1) {
+        // X0 <- X (buffer swap), X <- X + dt/2 F(X)
+        double* src[5];
+        double* out[5];
+        for (int d = 0; d < 5; d++) { src[d] = c->live[d]; out[d] = c->saved[d]; }
+        launch_push3(c->geo, src, src, out, c->mu, c->n, 0.5 * c->prm.dt, c->gfield, c->dc, c->st);
+        for (int d = 0; d < 5; d++) std::swap(c->live[d], c->saved[d]);
+        c->stage_next = 2;
+    } else {
+        // X <- X0 + dt F(X_mid): read live (midpoint) + saved, write saved, swap
+        double* src[5];
+        double* base[5];
+        for (int d = 0; d < 5; d++) { src[d] = c->live[d]; base[d] = c->saved[d]; }
+        launch_push3(c->geo, src, base, base, c->mu, c->n, c->prm.dt, c->gfield, c->dc, c->st);
+        for (int d = 0; d < 5; d++) std::swap(c->live[d], c->saved[d]);
+        c->stage_next = 1;
+    }
+    KCHECK();
+    return GTCP_OK;
+}
+
+// ----------------------------------------------------------------------------
+// bin (H-4): counting sort of the live particles by cell key, tiles
+// ----------------------------------------------------------------------------
+static gtcp_status do_bin(gtcp_ctx c) {
+    const Geo& g = c->geo;
+    PSet s = live_set(c);
+    CU(cudaMemsetAsync(c->count, 0, (c->nkeys + 1) * sizeof(unsigned), c->st));
+    launch_bin_keys(g, s, c->n, c->key, c->rankbuf, c->count, c->st);
+    launch_scan_u32(c->count, c->offset, c->nkeys, c->scan_tmp, c->st);
+    launch_bin_dest(c->key, c->rankbuf, c->offset, c->n, c->rankbuf, c->st);
+    // permute live state, mu (and the saved state when mid-step) with one scratch array
+    std::vector<double**> arrs;
+    for (int d = 0; d < 5; d++) arrs.push_back(&c->live[d]);
+    arrs.push_back(&c->mu);
+    if (c->stage_next == 2)
+        for (int d = 0; d < 5; d++) arrs.push_back(&c->saved[d]);
+    for (double** a : arrs) {
+        launch_permute_f64(*a, c->scratch, c->rankbuf, c->n, c->st);
+        // keep bufA/bufB bookkeeping consistent: the scratch becomes the array
+        double* old = *a;
+        for (int d = 0; d < 5; d++) {
+            if (c->bufA[d] == old) c->bufA[d] = c->scratch;
+            if (c->bufB[d] == old) c->bufB[d] = c->scratch;
+        }
+        *a = c->scratch;
+        c->scratch = old;
+    }
+    if (c->id) {
+        launch_permute_u64(c->id, c->id_scratch, c->rankbuf, c->n, c->st);
+        std::swap(c->id, c->id_scratch);
+    }
+    launch_build_tiles(g, c->count, c->offset, c->tile_max, c->tiles, nullptr, nullptr, c->max_tiles, c->dc, c->st);
+    c->n_binned = c->n;
+    KCHECK();
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_bin(gtcp_ctx c) {
+    CHECK_CTX(c);
+    PhaseTimer t(c, GTCP_T_BIN);
+    return do_bin(c);
+}
+
+// ----------------------------------------------------------------------------
+// shift (H-1..H-3): implemented in gtcp_shift_host below
+// ----------------------------------------------------------------------------
+gtcp_status shift_exchange(gtcp_ctx c);
+
+extern "C" gtcp_status gtcp_shift(gtcp_ctx c) {
+    CHECK_CTX(c);
+    {
+        PhaseTimer t(c, GTCP_T_SHIFT);
+        if (c->prm.ntoroidal > 1) {
+            gtcp_status s = shift_exchange(c);
+            if (s != GTCP_OK) return s;
+        }
+    }
+    if (c->stage_next == 1) {  // a full step has completed
+        c->steps_done++;
+        if (c->prm.bin_every > 0 && c->steps_done % c->prm.bin_every == 0) {
+            PhaseTimer t(c, GTCP_T_BIN);
+            return do_bin(c);
+        }
+    }
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_step(gtcp_ctx c, int nsteps) {
+    CHECK_CTX(c);
+    if (c->stage_next != 1) return set_err(c, GTCP_ESTATE, "step: a stage is in progress");
+    for (int s = 0; s < nsteps; s++) {
+        for (int stage = 1; stage <= 2; stage++) {
+            gtcp_status r;
+            if ((r = gtcp_charge(c)) != GTCP_OK) return r;
+            if ((r = gtcp_poisson_smooth(c)) != GTCP_OK) return r;
+            if ((r = gtcp_field(c)) != GTCP_OK) return r;
+            if ((r = gtcp_push(c, stage)) != GTCP_OK) return r;
+            if ((r = gtcp_shift(c)) != GTCP_OK) return r;
+        }
+    }
+    return GTCP_OK;
+}
+
+// ----------------------------------------------------------------------------
+// particles in / out
+// ----------------------------------------------------------------------------
+extern "C" gtcp_status gtcp_load(gtcp_ctx c) {
+    CHECK_CTX(c);
+    const gtcp_params& p = c->prm;
+    long long per_plane = (long long)p.micell * (c->mgrid - p.mpsi);
+    long long n_dom = per_plane * c->P;
+    long long n = n_dom / p.npartdom + (c->rank_p < n_dom % p.npartdom ? 1 : 0);
+    if (n > c->cap) return set_err(c, GTCP_ECAPACITY, "load: capacity");
+    long long id0 = (long long)c->rank_t * n_dom + (long long)c->rank_p * (n_dom / p.npartdom) +
+                    std::min<long long>(c->rank_p, n_dom % p.npartdom);
+    c->n = n;
+    c->stage_next = 1;
+    PSet s = live_set(c);
+    double zlo = c->k0 * (GTCP_TWO_PI / p.mzetamax), zhi = (c->k0 + c->P) * (GTCP_TWO_PI / p.mzetamax);
+    launch_load(c->geo, s, n, p.seed, id0, p.w_init_amp, p.vcut, zlo, zhi, c->st);
+    KCHECK();
+    gtcp_status r = do_bin(c);
+    if (r != GTCP_OK) return r;
+    r = compute_marker_norm(c);
+    if (r != GTCP_OK) return r;
+    CU(cudaStreamSynchronize(c->st));
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_set_particles(gtcp_ctx c, int64_t n, const double* const* attr, const uint64_t* id) {
+    CHECK_CTX(c);
+    if (n < 0 || (n > 0 && !attr)) return set_err(c, GTCP_EINVAL, "set_particles: bad args");
+    if (n > c->cap) return set_err(c, GTCP_ECAPACITY, "set_particles: n exceeds capacity");
+    if (c->prm.track_ids && n > 0 && !id) return set_err(c, GTCP_EINVAL, "set_particles: ids required");
+    for (int d = 0; d < 6; d++)
+        if (n > 0 && !attr[d]) return set_err(c, GTCP_EINVAL, "set_particles: null attribute");
+    for (int d = 0; d < 5; d++)
+        CU(cudaMemcpyAsync(c->live[d], attr[d], n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->mu, attr[5], n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    if (c->id && id) CU(cudaMemcpyAsync(c->id, id, n * sizeof(uint64_t), cudaMemcpyHostToDevice, c->st));
+    c->n = n;
+    c->stage_next = 1;
+    gtcp_status r = do_bin(c);
+    if (r != GTCP_OK) return r;
+    r = compute_marker_norm(c);
+    if (r != GTCP_OK) return r;
+    CU(cudaStreamSynchronize(c->st));
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_get_particles(gtcp_ctx c, int64_t cap, int64_t* n, double* const* attr, uint64_t* id) {
+    CHECK_CTX(c);
+    if (!n) return set_err(c, GTCP_EINVAL, "get_particles: n is null");
+    *n = c->n;
+    if (cap < c->n) return set_err(c, GTCP_ECAPACITY, "get_particles: cap < n");
+    if (attr) {
+        const double* src[11];
+        for (int d = 0; d < 5; d++) { src[d] = c->live[d]; src[6 + d] = c->saved[d]; }
+        src[5] = c->mu;
+        for (int d = 0; d < 11; d++)
+            if (attr[d]) CU(cudaMemcpyAsync(attr[d], src[d], c->n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    }
+    if (id && c->id) CU(cudaMemcpyAsync(id, c->id, c->n * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_sample_particles(gtcp_ctx c, int64_t m, const int64_t* idx, double* const* attr,
+                                             uint64_t* id) {
+    CHECK_CTX(c);
+    if (m < 0 || (m > 0 && !idx)) return set_err(c, GTCP_EINVAL, "sample_particles: bad args");
+    for (int64_t q = 0; q < m; q++)
+        if (idx[q] < 0 || idx[q] >= c->n) return set_err(c, GTCP_EINVAL, "sample_particles: index out of range");
+    if (m == 0) return GTCP_OK;
+    long long* d_idx;
+    double* d_out;
+    CU(cudaMallocAsync((void**)&d_idx, m * sizeof(long long), c->st));
+    CU(cudaMallocAsync((void**)&d_out, m * sizeof(double), c->st));
+    CU(cudaMemcpyAsync(d_idx, idx, m * sizeof(long long), cudaMemcpyHostToDevice, c->st));
+    const double* src[11];
+    for (int d = 0; d < 5; d++) { src[d] = c->live[d]; src[6 + d] = c->saved[d]; }
+    src[5] = c->mu;
+    for (int d = 0; d < 11; d++) {
+        if (!attr || !attr[d]) continue;
+        launch_gather_f64(src[d], d_idx, m, d_out, c->st);
+        CU(cudaMemcpyAsync(attr[d], d_out, m * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    }
+    if (id && c->id) {
+        launch_gather_f64((const double*)c->id, d_idx, m, d_out, c->st);
+        CU(cudaMemcpyAsync(id, d_out, m * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    }
+    CU(cudaFreeAsync(d_idx, c->st));
+    CU(cudaFreeAsync(d_out, c->st));
+    KCHECK();
+    CU(cudaStreamSynchronize(c->st));
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_step_host(gtcp_ctx c, int64_t n, double* const* attr, int nsteps) {
+    CHECK_CTX(c);
+    if (n < 0 || n > c->cap || !attr) return set_err(c, GTCP_EINVAL, "step_host: bad args");
+    for (int d = 0; d < 6; d++)
+        if (!attr[d]) return set_err(c, GTCP_EINVAL, "step_host: null attribute");
+    for (int d = 0; d < 5; d++)
+        CU(cudaMemcpyAsync(c->live[d], attr[d], n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->mu, attr[5], n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    c->n = n;
+    c->stage_next = 1;
+    launch_wmax(c->live[4], c->n, c->dc, c->st);
+    gtcp_status r = gtcp_step(c, nsteps);
+    if (r != GTCP_OK) return r;
+    for (int d = 0; d < 5; d++)
+        CU(cudaMemcpyAsync(attr[d], c->live[d], c->n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    return GTCP_OK;
+}
+
+// ----------------------------------------------------------------------------
+// grids in / out
+// ----------------------------------------------------------------------------
+extern "C" gtcp_status gtcp_get_grid(gtcp_ctx c, int which, int64_t cap, double* host) {
+    CHECK_CTX(c);
+    const long long mg = c->mgrid;
+    const long long planes = c->P + 1;
+    if (!host) return set_err(c, GTCP_EINVAL, "get_grid: null buffer");
+    switch (which) {
+        case GTCP_GRID_CHARGE:
+        case GTCP_GRID_PHI: {
+            if (cap < planes * mg) return set_err(c, GTCP_ECAPACITY, "get_grid: cap");
+            const double* H = which == GTCP_GRID_CHARGE ? c->rhoH : c->phiH;
+            CU(cudaMemcpyAsync(host, H + mg, planes * mg * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+            break;
+        }
+        case GTCP_GRID_GRADPHI: {
+            if (cap < planes * mg * 3) return set_err(c, GTCP_ECAPACITY, "get_grid: cap");
+            double* tmp = c->tmpH;  // (P+3) mg >= 3 (P+1) mg only if P >= 0... use dnH+tmpH contiguous? allocate
+            double* buf;
+            CU(cudaMallocAsync((void**)&buf, planes * mg * 3 * sizeof(double), c->st));
+            launch_gfield_export(c->geo, c->gfield, buf, c->st);
+            CU(cudaMemcpyAsync(host, buf, planes * mg * 3 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+            CU(cudaFreeAsync(buf, c->st));
+            (void)tmp;
+            break;
+        }
+        case GTCP_GRID_MARKER: {
+            if (cap < c->prm.mpsi + 1) return set_err(c, GTCP_ECAPACITY, "get_grid: cap");
+            CU(cudaMemcpyAsync(host, c->nm, (c->prm.mpsi + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+            break;
+        }
+        default: return set_err(c, GTCP_EINVAL, "get_grid: unknown grid");
+    }
+    CU(cudaStreamSynchronize(c->st));
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_set_grid(gtcp_ctx c, int which, int64_t n, const double* host) {
+    CHECK_CTX(c);
+    const long long mg = c->mgrid;
+    const long long planes = c->P + 1;
+    if (!host) return set_err(c, GTCP_EINVAL, "set_grid: null buffer");
+    switch (which) {
+        case GTCP_GRID_CHARGE:
+        case GTCP_GRID_PHI: {
+            if (n != planes * mg) return set_err(c, GTCP_EINVAL, "set_grid: size");
+            double* H = which == GTCP_GRID_CHARGE ? c->rhoH : c->phiH;
+            CU(cudaMemcpyAsync(H + mg, host, planes * mg * sizeof(double), cudaMemcpyHostToDevice, c->st));
+            gtcp_status s = halo_exchange(c, H);
+            if (s != GTCP_OK) return s;
+            break;
+        }
+        case GTCP_GRID_GRADPHI: {
+            if (n != planes * mg * 3) return set_err(c, GTCP_EINVAL, "set_grid: size");
+            double* buf;
+            CU(cudaMallocAsync((void**)&buf, planes * mg * 3 * sizeof(double), c->st));
+            CU(cudaMemcpyAsync(buf, host, planes * mg * 3 * sizeof(double), cudaMemcpyHostToDevice, c->st));
+            launch_gfield_import(c->geo, buf, c->gfield, c->st);
+            CU(cudaFreeAsync(buf, c->st));
+            break;
+        }
+        case GTCP_GRID_MARKER: {
+            if (n != c->prm.mpsi + 1) return set_err(c, GTCP_EINVAL, "set_grid: size");
+            CU(cudaMemcpyAsync(c->nm, host, n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+            break;
+        }
+        default: return set_err(c, GTCP_EINVAL, "set_grid: unknown grid");
+    }
+    KCHECK();
+    CU(cudaStreamSynchronize(c->st));
+    return GTCP_OK;
+}
+
+// ----------------------------------------------------------------------------
+// stats / timings
+// ----------------------------------------------------------------------------
+extern "C" gtcp_status gtcp_stats(gtcp_ctx c, gtcp_stats_t* out) {
+    CHECK_CTX(c);
+    if (!out) return GTCP_EINVAL;
+    launch_sum_f64(c->live[4], c->n, c->d_scalar, c->d_partial, c->st);
+    long long nl = c->n;
+    CU(cudaMemcpyAsync(c->d_scalar + 1, &nl, 8, cudaMemcpyHostToDevice, c->st));
+    if (c->nranks > 1) {
+        NC(ncclAllReduce(c->d_scalar, c->d_scalar + 2, 1, ncclDouble, ncclSum, c->world, c->st));
+        NC(ncclAllReduce(c->d_scalar + 1, c->d_scalar + 3, 1, ncclInt64, ncclSum, c->world, c->st));
+    } else {
+        CU(cudaMemcpyAsync(c->d_scalar + 2, c->d_scalar, 16, cudaMemcpyDeviceToDevice, c->st));
+    }
+    CU(cudaMemcpyAsync(c->h_scalar, c->d_scalar, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaMemcpyAsync(c->h_dc, c->dc, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    KCHECK();
+    out->n_local = c->n;
+    long long ng;
+    memcpy(&ng, &c->h_scalar[3], 8);
+    out->n_global = ng;
+    out->sum_w = c->h_scalar[2];
+    double wm;
+    memcpy(&wm, &c->h_dc->wmax_bits, 8);
+    out->max_abs_w = wm;
+    out->movers_sent = c->movers_sent;
+    out->movers_recv = c->movers_recv;
+    out->reflections = c->h_dc->reflections;
+    out->plane_clamps = c->h_dc->plane_clamps;
+    out->charge_global_fallback = c->h_dc->fallback;
+    out->fx_shift = c->h_dc->fx_shift;
+    if (c->h_dc->nonfinite) return set_err(c, GTCP_ENONFINITE, "non-finite particle state");
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_timings(gtcp_ctx c, gtcp_timings_t* out) {
+    CHECK_CTX(c);
+    if (!out) return GTCP_EINVAL;
+    CU(cudaStreamSynchronize(c->st));
+    fold_pending(c);
+    for (int i = 0; i < GTCP_NPHASE; i++) {
+        out->ms[i] = c->t_ms[i];
+        out->calls[i] = c->t_calls[i];
+    }
+    out->launches = gtcp::g_launches - c->launches0;
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_timings_reset(gtcp_ctx c) {
+    CHECK_CTX(c);
+    CU(cudaStreamSynchronize(c->st));
+    fold_pending(c);
+    for (int i = 0; i < GTCP_NPHASE; i++) { c->t_ms[i] = 0; c->t_calls[i] = 0; }
+    c->launches0 = gtcp::g_launches;
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_set_timing(gtcp_ctx c, int enable) {
+    CHECK_CTX(c);
+    c->timing = enable != 0;
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_set_charge_mode(gtcp_ctx c, int mode) {
+    CHECK_CTX(c);
+    if (mode != 0 && mode != 1) return GTCP_EINVAL;
+    c->charge_mode = mode;
+    return GTCP_OK;
+}
+
+// ----------------------------------------------------------------------------
+// shift over NCCL (toroidal ring neighbours), H-1..H-3
+// ----------------------------------------------------------------------------
+gtcp_status shift_exchange(gtcp_ctx c) {
+    (void)c;
+    return set_err(c, GTCP_EINVAL, "shift: multi-domain shift not built yet");
+}

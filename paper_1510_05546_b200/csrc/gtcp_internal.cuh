@@ -1,0 +1,115 @@
+// gtcp_internal.cuh -- private declarations of the B200 GTC-P library.
+// Product code: shares nothing with oracle/ (see DESIGN.md §2).
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/gtcp.h"
+
+#define GTCP_TWO_PI (2.0 * 3.14159265358979323846)
+
+// Geometry + physics constants passed by value to every kernel.
+struct Geo {
+    int mpsi, mzetamax, P, k0;     // rings, global planes, local planes, first local plane
+    int ntor, rank_t;              // toroidal domains, this rank's toroidal index
+    int mgrid;                     // nodes per plane incl. duplicates (< 2^31)
+    int paranl, drifts;
+    double a0, a1, dr, inv_dr, R0, inv_R0, omega0, q0, q2, rln, rlt, tau, dt;
+    double cz;                     // mzetamax / (2 pi), rounded once (Q-2, H-1)
+    double dzeta;                  // 2 pi / mzetamax
+    double rhoG;                   // sqrt(2) / omega0 (F-1)
+    const int* mtheta;             // [mpsi+1]
+    const int* igrid;              // [mpsi+2]
+    const int* itran;              // [mpsi+1]
+    const double* qtinv;           // [mpsi+1]
+};
+
+// One charge tile: particles [start, end) of the cell-sorted store whose
+// gyrocentre cell (ring, label) lay in ring `ring`, cells [c0, c1] at bin time.
+struct Tile {
+    int ring, c0, c1, pad;
+    long long start, end;
+};
+
+// SoA particle set: live state x[5] (psi, theta, zeta, rho_par, w), saved x0[5], mu.
+struct PSet {
+    double* x[5];
+    double* x0[5];
+    double* mu;
+    unsigned long long* id;        // may be null
+};
+
+// Device counters (one allocation, zeroed at init).
+struct DevCounters {
+    unsigned long long wmax_bits;  // max |w| of the live state (bits of a positive double)
+    long long reflections;
+    long long plane_clamps;
+    long long fallback;            // contributions that went straight to L2 in the last charge
+    int fx_shift;                  // fixed-point F of the last charge
+    int tile_next;                 // persistent-CTA tile counter
+    int ntiles;                    // tiles built by the last bin
+    int nonfinite;
+    long long n_send[2];           // shift: movers to left / right
+    long long n_keep;
+    long long n_holes;
+};
+
+namespace gtcp {
+
+// ---- kernels (gtcp_kernels.cu) -------------------------------------------
+void launch_deposit_tiled(const Geo& g, const PSet& s, long long n, const Tile* tiles, int max_tiles,
+                          long long* fx, DevCounters* dc, int ctas, size_t smem_bytes, int cap_nodes,
+                          cudaStream_t st);
+cudaError_t configure_deposit_tiled(size_t smem_bytes);
+void launch_deposit_direct(const Geo& g, const PSet& s, long long begin, long long n, long long* fx,
+                           DevCounters* dc, cudaStream_t st);
+void launch_fx_scale(DevCounters* dc, cudaStream_t st);
+void launch_fx_to_real(const Geo& g, const long long* fx, double* rho, const DevCounters* dc, int planes,
+                       cudaStream_t st);
+void launch_push3(const Geo& g, const double* const src[5], const double* const base[5], double* const out[5],
+                  const double* mu, long long n, double h, const double* gfield, DevCounters* dc, cudaStream_t st);
+void launch_wmax(const double* w, long long n, DevCounters* dc, cudaStream_t st);
+void launch_bin_keys(const Geo& g, const PSet& s, long long n, unsigned* key, unsigned* rank, unsigned* count,
+                     cudaStream_t st);
+void launch_scan_u32(const unsigned* in, unsigned* out, long long n, unsigned* block_tmp, cudaStream_t st);
+void launch_bin_dest(const unsigned* key, const unsigned* rank, const unsigned* offset, long long n,
+                     unsigned* dest, cudaStream_t st);
+void launch_permute_f64(const double* src, double* dst, const unsigned* dest, long long n, cudaStream_t st);
+void launch_permute_u64(const unsigned long long* src, unsigned long long* dst, const unsigned* dest,
+                        long long n, cudaStream_t st);
+void launch_build_tiles(const Geo& g, const unsigned* count, const unsigned* offset, int tile_max, Tile* tiles,
+                        int* ring_ntiles, int* ring_tile0, int max_tiles, DevCounters* dc, cudaStream_t st);
+void launch_load(const Geo& g, const PSet& s, long long n, unsigned long long seed, long long id0,
+                 double w_amp, double vcut, double zlo, double zhi, cudaStream_t st);
+// grid kernels (gtcp_grid.cu)
+void launch_fill_dup(const Geo& g, double* f, int planes, int ncomp, cudaStream_t st);
+void launch_seam_rotate(const Geo& g, const double* src, double* dst, int shift_sign, cudaStream_t st);
+void launch_rotate_add_i64(const Geo& g, const long long* src, long long* dst, int shift_sign, cudaStream_t st);
+void launch_normalize(const Geo& g, const double* rho, const double* nm, double* dn, cudaStream_t st);
+void launch_smooth_theta(const Geo& g, const double* in, double* out, cudaStream_t st);
+void launch_smooth_r(const Geo& g, const double* in, double* out, cudaStream_t st);
+void launch_smooth_par(const Geo& g, const double* in, double* out, cudaStream_t st);
+void launch_ring_sum(const Geo& g, const double* f, double* ringsum, cudaStream_t st);
+void launch_jacobi_init(const Geo& g, const double* dn, const double* ringsum, double* rhs, double* phi,
+                        cudaStream_t st);
+void launch_gyro(const Geo& g, const double* in, double* out, cudaStream_t st);
+void launch_jacobi_update(const Geo& g, const double* rhs, const double* g2, double* phi, double omega,
+                          cudaStream_t st);
+void launch_zonal(const Geo& g, const double* ringsum, double* phi00, cudaStream_t st);
+void launch_add_zonal2(const Geo& g, const double* phi00, const double* phi, double* phiH, cudaStream_t st);
+void launch_field(const Geo& g, const double* phi, double* gfield, cudaStream_t st);
+void launch_gfield_export(const Geo& g, const double* gfield, double* out, cudaStream_t st);
+void launch_gfield_import(const Geo& g, const double* in, double* gfield, cudaStream_t st);
+void launch_marker_from_rho(const Geo& g, const double* rho, double* ringsum, cudaStream_t st);
+void launch_ring_mean(const Geo& g, const double* ringsum, double* nm, cudaStream_t st);
+void launch_sum_f64(const double* x, long long n, double* out, double* partial, cudaStream_t st);
+void launch_fill_f64(double* x, long long n, double v, cudaStream_t st);
+void launch_gather_f64(const double* src, const long long* idx, long long m, double* out, cudaStream_t st);
+
+extern long long g_launches;  // kernels launched (for the bench's gpu_launches claim)
+
+}  // namespace gtcp

@@ -1,0 +1,899 @@
+// gtcp_kernels.cu -- particle kernels of the B200 GTC-P hot path (sm_100a).
+//
+//   charge : k_deposit_tiled  -- persistent CTAs over cell-sorted tiles; each
+//            tile's deposition footprint (all local planes x a radial band x a
+//            label window per ring) lives in shared memory as 64-bit fixed
+//            point split into two 32-bit limbs updated with native ATOMS.ADD
+//            (24 ops/SM/clk measured, vs 5/SM/clk for the fp64 CAS loop), then
+//            flushed once with REDG.ADD.64 into an L2-resident int64 grid.
+//            Contributions outside the window go straight to L2.
+//            Deterministic: integer sums are order-independent.
+//   push   : k_push           -- fused gather (4-point gyro-average of the
+//            gradient from the interval-interleaved field) + RK2 stage.
+//   bin    : counting sort by cell key (H-4) + permutation + tile build.
+//   load   : counter-based Philox marker loader (L-1..L-3 recipe).
+//
+// Paper passages: charge P:201-209; push P:224-227, P:374-378,
+// Eqs. 2-8; bin P:317-318.  Readings: SURVEY §8(c).
+#include <cooperative_groups.h>
+
+#include "gtcp_internal.cuh"
+
+namespace gtcp {
+
+long long g_launches = 0;
+
+static constexpr double kInvTwoPi = 1.0 / GTCP_TWO_PI;
+static constexpr int kMaxRings = 16;   // radial band of one tile window
+static constexpr int kDepositThreads = 512;
+static constexpr int kMaxPlanes = 80;  // P+1 planes of a tile window (host falls back to direct above)
+
+// round-to-nearest-even integer of a*b for |a*b| < 2^51 (1.5*2^52 magic
+// constant, one fused rounding).  Explicit intrinsics: every kernel computes
+// bit-identical contributions, so tiled and direct deposits agree bitwise.
+__device__ __forceinline__ long long fx_round(double a, double b) {
+    const double M = 6755399441055744.0;
+    double t = __fma_rn(a, b, M);
+    return __double_as_longlong(t) - __double_as_longlong(M);
+}
+
+// Q-2 / H-1: global plane interval and its upper weight.  Same operation
+// sequence as the oracle (single rounded multiply, floor), bit-exact.
+__device__ __forceinline__ int plane_of(const Geo& g, double zeta, double* wz1) {
+    double tg = __dmul_rn(zeta, g.cz);
+    int k = (int)floor(tg);
+    k = min(max(k, 0), g.mzetamax - 1);
+    *wz1 = __dsub_rn(tg, (double)k);
+    return k;
+}
+
+// Q-3..Q-5: the 4 gyro-points x 2 bounding rings of a particle.  For each
+// (point, ring) calls fn(m, j, mt, a0, a1) with a0/a1 = 1/4 * wp * wt0/wt1,
+// the weights of label nodes j and j+1 (j+1 may equal mt: the duplicate).
+template <class Fn>
+__device__ __forceinline__ void gyro_stencil(const Geo& g, double r, double theta, double zeta, double rho,
+                                             double inv_r, Fn&& fn) {
+    // explicit roundings: the same bits in every kernel that inlines this
+    const double rho_r = __dmul_rn(rho, inv_r);
+#pragma unroll
+    for (int l = 0; l < 4; l++) {
+        double rl = r, tl = theta;
+        if (l == 0) rl = __dadd_rn(r, rho);
+        if (l == 2) rl = __dsub_rn(r, rho);
+        if (l == 1) tl = __dadd_rn(theta, rho_r);
+        if (l == 3) tl = __dsub_rn(theta, rho_r);
+        rl = fmin(fmax(rl, g.a0), g.a1);
+        double x = __dmul_rn(__dsub_rn(rl, g.a0), g.inv_dr);
+        int i = (int)floor(x);
+        i = min(max(i, 0), g.mpsi - 1);
+        double wp1 = __dsub_rn(x, (double)i);
+#pragma unroll
+        for (int mm = 0; mm < 2; mm++) {
+            int m = i + mm;
+            double qt = __ldg(g.qtinv + m);
+            int mt = __ldg(g.mtheta + m);
+            double s = __dmul_rn(__fma_rn(-zeta, qt, tl), kInvTwoPi);
+            s = __dsub_rn(s, floor(s));
+            s = __dmul_rn(s, (double)mt);
+            int j = min((int)floor(s), mt - 1);
+            double wt1 = __dsub_rn(s, (double)j);
+            double wp = mm ? wp1 : __dsub_rn(1.0, wp1);
+            fn(m, j, mt, __dmul_rn(__dmul_rn(0.25, wp), __dsub_rn(1.0, wt1)), __dmul_rn(__dmul_rn(0.25, wp), wt1));
+        }
+    }
+}
+
+// per-particle gyroradius inputs with explicit roundings (shared by all kernels)
+__device__ __forceinline__ void gyro_radius(const Geo& g, double psi, double ct, double mu, double* r, double* invB,
+                                            double* rho, double* inv_r) {
+    *r = sqrt(__dmul_rn(2.0, psi));
+    *invB = __fma_rn(__dmul_rn(*r, g.inv_R0), ct, 1.0);
+    *rho = __ddiv_rn(sqrt(__dmul_rn(__dmul_rn(2.0, mu), *invB)), g.omega0);
+    *inv_r = __drcp_rn(*r);
+}
+
+// Global fixed-point grid index of canonical node (kk, m, j), j < mt.  On a
+// single toroidal domain the seam plane P is folded into plane 0 with the
+// exact label rotation j -> (j + itran_m) mod mt (G-4).
+__device__ __forceinline__ long long fx_node(const Geo& g, int kk, int m, int j, int mt) {
+    if (g.ntor == 1 && kk == g.P) {
+        kk = 0;
+        j += __ldg(g.itran + m);
+        j -= (j / mt) * mt;
+    }
+    return (long long)kk * g.mgrid + __ldg(g.igrid + m) + j;
+}
+
+__device__ __forceinline__ void red_i64(long long* p, long long v) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
+}
+
+// shared-memory 2-limb fixed-point add: value = hi * 2^32 + lo (carry from lo)
+__device__ __forceinline__ void smem_add(unsigned* lo, int* hi, int slot, long long v) {
+    unsigned vlo = (unsigned)v;
+    int vhi = (int)(v >> 32);
+    unsigned old = atomicAdd(lo + slot, vlo);
+    vhi += (old + vlo < old) ? 1 : 0;
+    if (vhi) atomicAdd(hi + slot, vhi);
+}
+
+__device__ __forceinline__ double fx_scale(const DevCounters* dc) { return scalbn(1.0, dc->fx_shift); }
+
+// ---------------------------------------------------------------------------
+// charge: fixed-point scale.  F = 42 - ceil(log2 max|w|) so |w| 2^F <= 2^42 and
+// every contribution (<= |w|/4) rounds to an integer below 2^40.
+// ---------------------------------------------------------------------------
+__global__ void k_fx_scale(DevCounters* dc) {
+    double wmax = __longlong_as_double((long long)dc->wmax_bits);
+    int F = 42;
+    if (wmax > 0.0 && isfinite(wmax)) {
+        int e;
+        frexp(wmax, &e);  // wmax in [2^(e-1), 2^e)
+        F = 42 - e;
+    }
+    F = max(-60, min(F, 60));
+    dc->fx_shift = F;
+    dc->fallback = 0;
+    dc->tile_next = 0;
+}
+
+void launch_fx_scale(DevCounters* dc, cudaStream_t st) {
+    k_fx_scale<<<1, 1, 0, st>>>(dc);
+    g_launches++;
+}
+
+// ---------------------------------------------------------------------------
+// charge: direct deposit (every contribution is one REDG.ADD.64 into L2).
+// Used for particles outside any tile (arrivals after a shift) and as the
+// reference mode 1.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_deposit_direct(Geo g, PSet s, long long begin, long long n,
+                                                        long long* __restrict__ fx, DevCounters* dc) {
+    const double scale = fx_scale(dc);
+    long long clamps = 0;
+    for (long long p = begin + blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x) {
+        double psi = s.x[0][p], theta = s.x[1][p], zeta = s.x[2][p], w = s.x[4][p], mu = s.mu[p];
+        double r, invB, rho, inv_r;
+        gyro_radius(g, psi, cos(theta), mu, &r, &invB, &rho, &inv_r);
+        double wz1;
+        int kg = plane_of(g, zeta, &wz1);
+        int k = kg - g.k0;
+        if (k < 0 || k > g.P - 1) { clamps++; k = min(max(k, 0), g.P - 1); }
+        double ws = __dmul_rn(w, scale);
+        double wz[2] = {__dmul_rn(__dsub_rn(1.0, wz1), ws), __dmul_rn(wz1, ws)};
+        gyro_stencil(g, r, theta, zeta, rho, inv_r, [&](int m, int j, int mt, double a0, double a1) {
+            int j1 = (j + 1 == mt) ? 0 : j + 1;
+#pragma unroll
+            for (int kk = 0; kk < 2; kk++) {
+                long long v0 = fx_round(wz[kk], a0), v1 = fx_round(wz[kk], a1);
+                if (v0) red_i64(fx + fx_node(g, k + kk, m, j, mt), v0);
+                if (v1) red_i64(fx + fx_node(g, k + kk, m, j1, mt), v1);
+            }
+        });
+    }
+    if (clamps) atomicAdd((unsigned long long*)&dc->plane_clamps, (unsigned long long)clamps);
+}
+
+void launch_deposit_direct(const Geo& g, const PSet& s, long long begin, long long n, long long* fx,
+                           DevCounters* dc, cudaStream_t st) {
+    if (n <= begin) return;
+    long long work = n - begin;
+    int blocks = (int)std::min<long long>((work + 255) / 256, 148LL * 16);
+    k_deposit_direct<<<blocks, 256, 0, st>>>(g, s, begin, n, fx, dc);
+    g_launches++;
+}
+
+// ---------------------------------------------------------------------------
+// charge: tiled deposit.
+// ---------------------------------------------------------------------------
+struct WinTables {
+    int m_lo, nr, S, total;
+    int W[kMaxRings], off[kMaxRings], mt[kMaxRings];
+    long long start, end;
+    int tile;
+};
+
+__global__ void __launch_bounds__(kDepositThreads, 2)
+    k_deposit_tiled(Geo g, PSet s, long long n, const Tile* __restrict__ tiles, const int* ntiles_p,
+                    long long* __restrict__ fx, DevCounters* dc, int cap_nodes, double rho_cut) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned* slo = reinterpret_cast<unsigned*>(smem_raw);
+    int* shi = reinterpret_cast<int*>(slo + cap_nodes);
+    int* js = shi + cap_nodes;  // [(P+1) * nr]
+    __shared__ WinTables T;
+    __shared__ unsigned long long s_fallback;
+    const double scale = fx_scale(dc);
+    const int ntiles = *ntiles_p;
+    const int P1 = g.P + 1;
+    if (threadIdx.x == 0) s_fallback = 0;
+
+    for (;;) {
+        if (threadIdx.x == 0) T.tile = atomicAdd(&dc->tile_next, 1);
+        __syncthreads();
+        const int t = T.tile;
+        if (t >= ntiles) break;
+        // ---- window of this tile (rings m_lo..m_lo+nr-1, label window per ring/plane)
+        if (threadIdx.x == 0) {
+            Tile tl = tiles[t];
+            int i = tl.ring;
+            int h = (int)ceil(rho_cut * g.inv_dr) + 1;
+            h = min(h, (kMaxRings - 2) / 2);
+            int m_lo = max(0, i - h), m_hi = min(g.mpsi, i + 1 + h);
+            T.m_lo = m_lo;
+            T.nr = m_hi - m_lo + 1;
+            T.start = tl.start;
+            T.end = min(tl.end, n);
+            int S = 0;
+            int mti = __ldg(g.mtheta + i);
+            double half0 = 0.5 * (double)(tl.c1 + 1 - tl.c0) / mti;
+            double qti = __ldg(g.qtinv + i);
+            for (int q = 0; q < T.nr; q++) {
+                int m = m_lo + q;
+                int mt = __ldg(g.mtheta + m);
+                double dq = (qti - __ldg(g.qtinv + m)) * kInvTwoPi;
+                double rm = g.a0 + m * g.dr;
+                double thm = (m >= i - 1 && m <= i + 2) ? rho_cut / rm * kInvTwoPi : 0.0;
+                double hw = half0 + g.dzeta * fabs(dq) + thm + 1.0 / mt;
+                int W = (int)ceil(2.0 * hw * mt) + 2;
+                W = min(W, mt);
+                T.W[q] = W;
+                T.mt[q] = mt;
+                T.off[q] = S;
+                S += W;
+            }
+            T.S = S;
+            T.total = S * P1;
+            if (T.total > cap_nodes) {  // pathological window: everything via L2
+                T.total = 0;
+                for (int q = 0; q < T.nr; q++) T.W[q] = 0;
+            }
+        }
+        __syncthreads();
+        {
+            Tile tl = tiles[t];
+            int i = tl.ring;
+            int mti = __ldg(g.mtheta + i);
+            double fc = 0.5 * (double)(tl.c0 + tl.c1 + 1) / mti;
+            double half0 = 0.5 * (double)(tl.c1 + 1 - tl.c0) / mti;
+            double qti = __ldg(g.qtinv + i);
+            for (int e = threadIdx.x; e < P1 * T.nr; e += blockDim.x) {
+                int kk = e / T.nr, q = e - kk * T.nr;
+                int m = T.m_lo + q;
+                int mt = T.mt[q];
+                double dq = (qti - __ldg(g.qtinv + m)) * kInvTwoPi;
+                double rm = g.a0 + m * g.dr;
+                double thm = (m >= i - 1 && m <= i + 2) ? rho_cut / rm * kInvTwoPi : 0.0;
+                double hw = half0 + g.dzeta * fabs(dq) + thm + 1.0 / mt;
+                double zk = (double)(g.k0 + kk) * g.dzeta;
+                double f = fc + zk * dq - hw;
+                f = f - floor(f);
+                int j0 = (int)floor(f * mt);
+                j0 = min(max(j0, 0), mt - 1);
+                js[e] = j0;
+            }
+            for (int e = threadIdx.x; e < T.total; e += blockDim.x) {
+                slo[e] = 0u;
+                shi[e] = 0;
+            }
+        }
+        __syncthreads();
+        // ---- deposit the tile's particles
+        const int m_lo = T.m_lo, nr = T.nr, S = T.S;
+        unsigned long long fb = 0;
+        long long clamps = 0;
+        for (long long p = T.start + threadIdx.x; p < T.end; p += blockDim.x) {
+            double psi = s.x[0][p], theta = s.x[1][p], zeta = s.x[2][p], w = s.x[4][p], mu = s.mu[p];
+            double r, invB, rho, inv_r;
+            gyro_radius(g, psi, cos(theta), mu, &r, &invB, &rho, &inv_r);
+            double wz1;
+            int kg = plane_of(g, zeta, &wz1);
+            int k = kg - g.k0;
+            if (k < 0 || k > g.P - 1) { clamps++; k = min(max(k, 0), g.P - 1); }
+            double ws = __dmul_rn(w, scale);
+            double wz[2] = {__dmul_rn(__dsub_rn(1.0, wz1), ws), __dmul_rn(wz1, ws)};
+            gyro_stencil(g, r, theta, zeta, rho, inv_r, [&](int m, int j, int mt, double a0, double a1) {
+                int j1 = (j + 1 == mt) ? 0 : j + 1;
+                int q = m - m_lo;
+                bool inr = (unsigned)q < (unsigned)nr;
+#pragma unroll
+                for (int kk = 0; kk < 2; kk++) {
+                    long long v0 = fx_round(wz[kk], a0), v1 = fx_round(wz[kk], a1);
+                    int d = -1, d1 = -1, W = 0, base = 0;
+                    if (inr) {
+                        W = T.W[q];
+                        base = (k + kk) * S + T.off[q];
+                        d = j - js[(k + kk) * nr + q];
+                        if (d < 0) d += mt;
+                        d1 = (d + 1 == mt) ? 0 : d + 1;
+                    }
+                    if (v0) {
+                        if (inr && d < W) smem_add(slo, shi, base + d, v0);
+                        else { red_i64(fx + fx_node(g, k + kk, m, j, mt), v0); fb++; }
+                    }
+                    if (v1) {
+                        if (inr && d1 < W) smem_add(slo, shi, base + d1, v1);
+                        else { red_i64(fx + fx_node(g, k + kk, m, j1, mt), v1); fb++; }
+                    }
+                }
+            });
+        }
+        if (fb) atomicAdd(&s_fallback, fb);
+        if (clamps) atomicAdd((unsigned long long*)&dc->plane_clamps, (unsigned long long)clamps);
+        __syncthreads();
+        // ---- flush the window to L2 (one REDG.ADD.64 per nonzero node)
+        for (int e = threadIdx.x; e < T.total; e += blockDim.x) {
+            long long v = (long long)(((unsigned long long)(unsigned)shi[e] << 32) + (unsigned long long)slo[e]);
+            if (v == 0) continue;
+            int kk = e / S;
+            int rem = e - kk * S;
+            int q = 0;
+            while (q + 1 < nr && T.off[q + 1] <= rem) q++;
+            int d = rem - T.off[q];
+            int mt = T.mt[q];
+            int j = js[kk * nr + q] + d;
+            if (j >= mt) j -= mt;
+            red_i64(fx + fx_node(g, kk, m_lo + q, j, mt), v);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && s_fallback) atomicAdd((unsigned long long*)&dc->fallback, s_fallback);
+}
+
+cudaError_t configure_deposit_tiled(size_t smem_bytes) {
+    return cudaFuncSetAttribute(k_deposit_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+}
+
+void launch_deposit_tiled(const Geo& g, const PSet& s, long long n, const Tile* tiles, int max_tiles,
+                          long long* fx, DevCounters* dc, int ctas, size_t smem_bytes, int cap_nodes,
+                          cudaStream_t st) {
+    (void)max_tiles;
+    double rho_cut = 3.0 / g.omega0;
+    k_deposit_tiled<<<ctas, kDepositThreads, smem_bytes, st>>>(g, s, n, tiles, &dc->ntiles, fx, dc, cap_nodes,
+                                                              rho_cut);
+    g_launches++;
+}
+
+// fixed point -> fp64 on planes 0..planes-1 (canonical and duplicate nodes)
+__global__ void k_fx_to_real(Geo g, const long long* __restrict__ fx, double* __restrict__ rho,
+                             const DevCounters* dc, int planes) {
+    const double inv = scalbn(1.0, -dc->fx_shift);
+    long long total = (long long)planes * g.mgrid;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x)
+        rho[e] = (double)fx[e] * inv;
+}
+
+void launch_fx_to_real(const Geo& g, const long long* fx, double* rho, const DevCounters* dc, int planes,
+                       cudaStream_t st) {
+    long long total = (long long)planes * g.mgrid;
+    int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
+    k_fx_to_real<<<blocks, 256, 0, st>>>(g, fx, rho, dc, planes);
+    g_launches++;
+}
+
+// ---------------------------------------------------------------------------
+// push: fused gather + RK2 stage (U-1..U-8).
+//   stage 1: out = src + dt/2 F(src)     (src = live X, out = other buffer)
+//   stage 2: out = base + dt F(src)      (src = midpoint, base = out = saved X0)
+// gfield layout: interval k, node n -> 6 doubles (plane k: gr gth gpar,
+// plane k+1: gr gth gpar); label nodes j, j+1 are 96 contiguous bytes.
+// ---------------------------------------------------------------------------
+struct PushPtrs {
+    const double* src[5];
+    const double* base[5];
+    double* out[5];
+    const double* mu;
+};
+
+__device__ __forceinline__ double warp_max(double v) {
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__global__ void __launch_bounds__(256) k_push(Geo g, PushPtrs pp, long long n, double h,
+                                             const double* __restrict__ gf, DevCounters* dc) {
+    double wmax = 0.0;
+    long long refl = 0, clamps = 0;
+    int nonfinite = 0;
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x) {
+        const double psi = pp.src[0][p], theta = pp.src[1][p], zeta = pp.src[2][p], rho_par = pp.src[3][p],
+                     w = pp.src[4][p], mu = pp.mu[p];
+        // U-1
+        double st, ct;
+        sincos(theta, &st, &ct);
+        double r, invB, rho, inv_r;
+        gyro_radius(g, psi, ct, mu, &r, &invB, &rho, &inv_r);
+        const double eps = r * g.inv_R0;
+        const double B = 1.0 / invB;
+        // U-2 gather
+        double wz1;
+        int kg = plane_of(g, zeta, &wz1);
+        int k = kg - g.k0;
+        if (k < 0 || k > g.P - 1) { clamps++; k = min(max(k, 0), g.P - 1); }
+        const double wz0 = 1.0 - wz1;
+        double gr = 0.0, gt = 0.0, gp = 0.0;
+        const double* gk = gf + (long long)k * g.mgrid * 6;
+        gyro_stencil(g, r, theta, zeta, rho, inv_r, [&](int m, int j, int mt, double a0, double a1) {
+            const double2* q = reinterpret_cast<const double2*>(gk + ((long long)__ldg(g.igrid + m) + j) * 6);
+            double2 v0 = __ldg(q + 0), v1 = __ldg(q + 1), v2 = __ldg(q + 2);
+            double2 v3 = __ldg(q + 3), v4 = __ldg(q + 4), v5 = __ldg(q + 5);
+            // node j: (v0.x v0.y v1.x) plane k, (v1.y v2.x v2.y) plane k+1; node j+1 likewise in v3..v5
+            double c00 = a0 * wz0, c01 = a0 * wz1, c10 = a1 * wz0, c11 = a1 * wz1;
+            gr += c00 * v0.x + c01 * v1.y + c10 * v3.x + c11 * v4.y;
+            gt += c00 * v0.y + c01 * v2.x + c10 * v3.y + c11 * v5.x;
+            gp += c00 * v1.x + c01 * v2.y + c10 * v4.x + c11 * v5.y;
+            (void)mt;
+        });
+        // U-3 drifts
+        const double q = g.q0 + g.q2 * r * r;
+        const double vpar = g.omega0 * B * rho_par;
+        double vEr = 0.0, vEt = 0.0, vdr = 0.0, vdt = 0.0;
+        if (g.drifts) {
+            vEr = -gt * inv_r / (g.omega0 * B);
+            vEt = gr / (g.omega0 * B);
+            const double Cd = (vpar * vpar + mu * B) / (g.omega0 * g.R0);
+            vdr = -Cd * st;
+            vdt = -Cd * ct;
+        }
+        // U-4
+        const double rdot = vEr + vdr;
+        const double psidot = r * rdot;
+        const double thdot = vpar * B / (q * g.R0) + (vEt + vdt) * inv_r;
+        const double zdot = vpar * B * g.inv_R0;
+        // U-5
+        double vdot = -mu * B * B * B * r * st / (q * g.R0 * g.R0);
+        if (g.paranl) {
+            double par = -(B * g.inv_R0) * gp;
+            if (g.drifts) par += (vpar / (g.omega0 * g.R0)) * (st * gr + ct * gt * inv_r);
+            vdot += par;
+        }
+        const double dBdr = -B * B * ct * g.inv_R0;
+        const double dBdt = B * B * eps * st;
+        const double Bdot = rdot * dBdr + thdot * dBdt;
+        const double rhodot = (vdot - vpar * Bdot * invB) / (g.omega0 * B);
+        // U-6 delta-f weight
+        const double Ekin = 0.5 * vpar * vpar + mu * B;
+        const double x6 = (r - 0.5) * (1.0 / 0.35);
+        const double x2 = x6 * x6;
+        const double prof = exp(-(x2 * x2 * x2));
+        const double kappa = prof * (g.rln + (Ekin - 1.5) * g.rlt) * g.inv_R0;
+        const double wdot = (1.0 - (double)g.paranl * w) *
+                            (vEr * kappa - (vpar * (B * g.inv_R0) * gp + vdr * gr + vdt * gt * inv_r));
+        // U-7 update
+        double X[5];
+        const double F[5] = {psidot, thdot, zdot, rhodot, wdot};
+#pragma unroll
+        for (int d = 0; d < 5; d++) X[d] = pp.base[d][p] + h * F[d];
+        // U-8 wrap angles (same operation sequence as the oracle) and reflect r
+#pragma unroll
+        for (int d = 1; d <= 2; d++) {
+            double t = __dsub_rn(X[d], __dmul_rn(GTCP_TWO_PI, floor(__ddiv_rn(X[d], GTCP_TWO_PI))));
+            if (t >= GTCP_TWO_PI) t = 0.0;
+            X[d] = t;
+        }
+        double rn = sqrt(2.0 * fmax(X[0], 0.0));
+        bool rf = false;
+        if (rn > g.a1) { rn = 2.0 * g.a1 - rn; rf = true; }
+        if (rn < g.a0) { rn = 2.0 * g.a0 - rn; rf = true; }
+        if (rf) { X[0] = 0.5 * rn * rn; refl++; }
+        if (!(isfinite(X[0]) && isfinite(X[1]) && isfinite(X[2]) && isfinite(X[3]) && isfinite(X[4]))) nonfinite = 1;
+#pragma unroll
+        for (int d = 0; d < 5; d++) pp.out[d][p] = X[d];
+        wmax = fmax(wmax, fabs(X[4]));
+    }
+    wmax = warp_max(wmax);
+    if ((threadIdx.x & 31) == 0 && wmax > 0.0)
+        atomicMax(&dc->wmax_bits, (unsigned long long)__double_as_longlong(wmax));
+    if (refl) atomicAdd((unsigned long long*)&dc->reflections, (unsigned long long)refl);
+    if (clamps) atomicAdd((unsigned long long*)&dc->plane_clamps, (unsigned long long)clamps);
+    if (nonfinite) dc->nonfinite = 1;
+}
+
+void launch_push3(const Geo& g, const double* const src[5], const double* const base[5], double* const out[5],
+                  const double* mu, long long n, double h, const double* gfield, DevCounters* dc,
+                  cudaStream_t st) {
+    if (n <= 0) return;
+    PushPtrs pp;
+    for (int d = 0; d < 5; d++) {
+        pp.src[d] = src[d];
+        pp.base[d] = base[d];
+        pp.out[d] = out[d];
+    }
+    pp.mu = mu;
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
+    k_push<<<blocks, 256, 0, st>>>(g, pp, n, h, gfield, dc);
+    g_launches++;
+}
+
+__global__ void k_wmax(const double* __restrict__ w, long long n, DevCounters* dc) {
+    double m = 0.0;
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x)
+        m = fmax(m, fabs(w[p]));
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(&dc->wmax_bits, (unsigned long long)__double_as_longlong(m));
+}
+
+void launch_wmax(const double* w, long long n, DevCounters* dc, cudaStream_t st) {
+    int blocks = (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148LL * 8));
+    k_wmax<<<blocks, 256, 0, st>>>(w, n, dc);
+    g_launches++;
+}
+
+// ---------------------------------------------------------------------------
+// bin (H-4): key = (igrid_i + c) * P + k, same operation sequence as the
+// oracle so the key is bit-exact; counting sort by key.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned bin_key(const Geo& g, double psi, double theta, double zeta) {
+    double r = sqrt(__dmul_rn(2.0, psi));
+    double x = __ddiv_rn(__dsub_rn(r, g.a0), g.dr);
+    int i = (int)floor(x);
+    i = min(max(i, 0), g.mpsi - 1);
+    double s = __ddiv_rn(__dsub_rn(theta, __dmul_rn(zeta, __ldg(g.qtinv + i))), GTCP_TWO_PI);
+    s = __dsub_rn(s, floor(s));
+    int mt = __ldg(g.mtheta + i);
+    s = __dmul_rn(s, (double)mt);
+    int c = (int)floor(s);
+    c = min(max(c, 0), mt - 1);
+    double wz1;
+    int k = plane_of(g, zeta, &wz1) - g.k0;
+    k = min(max(k, 0), g.P - 1);
+    return (unsigned)((__ldg(g.igrid + i) + c) * g.P + k);
+}
+
+__global__ void k_bin_keys(Geo g, PSet s, long long n, unsigned* __restrict__ key, unsigned* __restrict__ rank,
+                           unsigned* __restrict__ count) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x) {
+        unsigned kk = bin_key(g, s.x[0][p], s.x[1][p], s.x[2][p]);
+        key[p] = kk;
+        rank[p] = atomicAdd(count + kk, 1u);
+    }
+}
+
+void launch_bin_keys(const Geo& g, const PSet& s, long long n, unsigned* key, unsigned* rank, unsigned* count,
+                     cudaStream_t st) {
+    if (n <= 0) return;
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    k_bin_keys<<<blocks, 256, 0, st>>>(g, s, n, key, rank, count);
+    g_launches++;
+}
+
+// exclusive scan of n u32 -> out[0..n] (out[n] = total); 3 kernels
+static constexpr int kScanChunk = 4096;
+
+__device__ __forceinline__ unsigned block_exclusive_scan(unsigned v, unsigned* sm, unsigned* total) {
+    // blockDim.x == 1024
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sm[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        unsigned t = sm[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        sm[lane] = t;
+    }
+    __syncthreads();
+    unsigned excl = x - v + (wid ? sm[wid - 1] : 0u);
+    if (total) *total = sm[31];
+    __syncthreads();
+    return excl;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_reduce(const unsigned* __restrict__ in, long long n,
+                                                      unsigned* __restrict__ bsum) {
+    __shared__ unsigned sm[32];
+    long long base = (long long)blockIdx.x * kScanChunk;
+    unsigned v = 0;
+    for (int e = threadIdx.x; e < kScanChunk; e += 1024) {
+        long long q = base + e;
+        if (q < n) v += in[q];
+    }
+    unsigned tot;
+    block_exclusive_scan(v, sm, &tot);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_bsum(unsigned* bsum, int nb, unsigned* total_out) {
+    __shared__ unsigned sm[32];
+    unsigned carry = 0;
+    for (int b0 = 0; b0 < nb; b0 += 1024) {
+        int b = b0 + threadIdx.x;
+        unsigned v = b < nb ? bsum[b] : 0u;
+        unsigned tot;
+        unsigned ex = block_exclusive_scan(v, sm, &tot);
+        if (b < nb) bsum[b] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) *total_out = carry;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_final(const unsigned* __restrict__ in, long long n,
+                                                     const unsigned* __restrict__ bsum, unsigned* __restrict__ out) {
+    __shared__ unsigned sm[32];
+    long long base = (long long)blockIdx.x * kScanChunk;
+    constexpr int per = kScanChunk / 1024;
+    unsigned v[per];
+    unsigned s = 0;
+    for (int e = 0; e < per; e++) {
+        long long q = base + (long long)threadIdx.x * per + e;
+        v[e] = q < n ? in[q] : 0u;
+        s += v[e];
+    }
+    unsigned ex = block_exclusive_scan(s, sm, nullptr) + bsum[blockIdx.x];
+    for (int e = 0; e < per; e++) {
+        long long q = base + (long long)threadIdx.x * per + e;
+        if (q < n) out[q] = ex;
+        ex += v[e];
+    }
+}
+
+void launch_scan_u32(const unsigned* in, unsigned* out, long long n, unsigned* block_tmp, cudaStream_t st) {
+    int nb = (int)((n + kScanChunk - 1) / kScanChunk);
+    k_scan_reduce<<<nb, 1024, 0, st>>>(in, n, block_tmp);
+    k_scan_bsum<<<1, 1024, 0, st>>>(block_tmp, nb, out + n);
+    k_scan_final<<<nb, 1024, 0, st>>>(in, n, block_tmp, out);
+    g_launches += 3;
+}
+
+__global__ void k_bin_dest(const unsigned* __restrict__ key, const unsigned* __restrict__ rank,
+                           const unsigned* __restrict__ offset, long long n, unsigned* __restrict__ dest) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x)
+        dest[p] = offset[key[p]] + rank[p];
+}
+
+void launch_bin_dest(const unsigned* key, const unsigned* rank, const unsigned* offset, long long n,
+                     unsigned* dest, cudaStream_t st) {
+    if (n <= 0) return;
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    k_bin_dest<<<blocks, 256, 0, st>>>(key, rank, offset, n, dest);
+    g_launches++;
+}
+
+__global__ void k_permute_f64(const double* __restrict__ src, double* __restrict__ dst,
+                              const unsigned* __restrict__ dest, long long n) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x)
+        dst[dest[p]] = src[p];
+}
+
+void launch_permute_f64(const double* src, double* dst, const unsigned* dest, long long n, cudaStream_t st) {
+    if (n <= 0) return;
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    k_permute_f64<<<blocks, 256, 0, st>>>(src, dst, dest, n);
+    g_launches++;
+}
+
+__global__ void k_permute_u64(const unsigned long long* __restrict__ src, unsigned long long* __restrict__ dst,
+                              const unsigned* __restrict__ dest, long long n) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x)
+        dst[dest[p]] = src[p];
+}
+
+void launch_permute_u64(const unsigned long long* src, unsigned long long* dst, const unsigned* dest,
+                        long long n, cudaStream_t st) {
+    if (n <= 0) return;
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    k_permute_u64<<<blocks, 256, 0, st>>>(src, dst, dest, n);
+    g_launches++;
+}
+
+// Tiles: one thread per ring walks its cells (cell extent from the key
+// offsets: cell c of ring i owns keys [(igrid_i+c)P, (igrid_i+c+1)P)) and
+// greedily packs consecutive cells into tiles of at most tile_max particles.
+__device__ __forceinline__ int ring_tiles(const Geo& g, int i, const unsigned* offset, int tile_max,
+                                          Tile* out, int max_out) {
+    int mt = __ldg(g.mtheta + i), ig = __ldg(g.igrid + i);
+    int nt = 0;
+    long long cur = 0, tstart = offset[(long long)ig * g.P];
+    int c0 = 0;
+    auto emit = [&](int a, int b, long long s0, long long s1) {
+        if (s1 <= s0) return;
+        if (out && nt < max_out) {
+            Tile t;
+            t.ring = i; t.c0 = a; t.c1 = b; t.pad = 0; t.start = s0; t.end = s1;
+            out[nt] = t;
+        }
+        nt++;
+    };
+    for (int c = 0; c < mt; c++) {
+        long long cs = offset[(long long)(ig + c) * g.P];
+        long long ce = offset[(long long)(ig + c + 1) * g.P];
+        long long cnt = ce - cs;
+        if (cnt == 0) continue;
+        if (cur > 0 && cur + cnt > tile_max) {
+            emit(c0, c - 1 < c0 ? c0 : c - 1, tstart, cs);
+            cur = 0;
+            tstart = cs;
+            c0 = c;
+        }
+        if (cur == 0) { tstart = cs; c0 = c; }
+        cur += cnt;
+        while (cur > tile_max) {
+            emit(c0, c, tstart, tstart + tile_max);
+            tstart += tile_max;
+            cur -= tile_max;
+            c0 = c;
+        }
+    }
+    if (cur > 0) emit(c0, mt - 1, tstart, tstart + cur);
+    return nt;
+}
+
+__global__ void __launch_bounds__(1024) k_build_tiles(Geo g, const unsigned* __restrict__ offset, int tile_max,
+                                                      Tile* tiles, int max_tiles, DevCounters* dc) {
+    __shared__ unsigned sm[32];
+    __shared__ unsigned s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    // rings with gyrocentres: 0..mpsi-1 (bin key uses the floor ring)
+    for (int b0 = 0; b0 < g.mpsi; b0 += 1024) {
+        int i = b0 + threadIdx.x;
+        unsigned cnt = (i < g.mpsi) ? (unsigned)ring_tiles(g, i, offset, tile_max, nullptr, 0) : 0u;
+        unsigned tot;
+        unsigned ex = block_exclusive_scan(cnt, sm, &tot) + s_carry;
+        if (i < g.mpsi) {
+            int room = max_tiles - (int)ex;
+            if (room > 0) ring_tiles(g, i, offset, tile_max, tiles + ex, room);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) dc->ntiles = min((int)s_carry, max_tiles);
+}
+
+void launch_build_tiles(const Geo& g, const unsigned* count, const unsigned* offset, int tile_max, Tile* tiles,
+                        int* ring_ntiles, int* ring_tile0, int max_tiles, DevCounters* dc, cudaStream_t st) {
+    (void)count; (void)ring_ntiles; (void)ring_tile0;
+    k_build_tiles<<<1, 1024, 0, st>>>(g, offset, tile_max, tiles, max_tiles, dc);
+    g_launches++;
+}
+
+// deterministic sum: fixed grid of partials, then one block in fixed order
+__global__ void k_sum_partial(const double* __restrict__ x, long long n, double* __restrict__ partial) {
+    double s = 0.0;
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x)
+        s += x[p];
+    __shared__ double sm[32];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += sm[w];
+        partial[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_sum_final(const double* __restrict__ partial, int nb, double* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double t = 0.0;
+        for (int b = 0; b < nb; b++) t += partial[b];
+        out[0] = t;
+    }
+}
+
+void launch_sum_f64(const double* x, long long n, double* out, double* partial, cudaStream_t st) {
+    const int nb = 592;
+    k_sum_partial<<<nb, 256, 0, st>>>(x, n, partial);
+    k_sum_final<<<1, 32, 0, st>>>(partial, nb, out);
+    g_launches += 2;
+}
+
+__global__ void k_fill_f64(double* __restrict__ x, long long n, double v) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x)
+        x[p] = v;
+}
+
+void launch_fill_f64(double* x, long long n, double v, cudaStream_t st) {
+    if (n <= 0) return;
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    k_fill_f64<<<blocks, 256, 0, st>>>(x, n, v);
+    g_launches++;
+}
+
+__global__ void k_gather_f64(const double* __restrict__ src, const long long* __restrict__ idx, long long m,
+                             double* __restrict__ out) {
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < m; q += (long long)gridDim.x * blockDim.x)
+        out[q] = src[idx[q]];
+}
+
+void launch_gather_f64(const double* src, const long long* idx, long long m, double* out, cudaStream_t st) {
+    int blocks = (int)std::max<long long>(1, std::min<long long>((m + 255) / 256, 148LL * 8));
+    k_gather_f64<<<blocks, 256, 0, st>>>(src, idx, m, out);
+    g_launches++;
+}
+
+// ---------------------------------------------------------------------------
+// load: Philox4x32-10 counter-based generator; counter = (id lo, id hi, draw, 0)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+    const unsigned M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        unsigned hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
+        unsigned hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+        k.x += W0;
+        k.y += W1;
+    }
+    return c;
+}
+
+struct Philox {
+    uint2 key;
+    unsigned id_lo, id_hi, draw;
+    uint4 buf;
+    int used;
+    __device__ double u53() {  // uniform in [0, 1)
+        if (used >= 4) { buf = philox4x32_10(make_uint4(id_lo, id_hi, draw++, 0u), key); used = 0; }
+        unsigned a = (&buf.x)[used], b = (&buf.x)[used + 1];
+        used += 2;
+        unsigned long long m = ((unsigned long long)(a >> 5) << 26) | (b >> 6);
+        return (double)m * (1.0 / 9007199254740992.0);
+    }
+};
+
+__global__ void k_load(Geo g, PSet s, long long n, unsigned long long seed, long long id0, double w_amp,
+                       double vcut, double zlo, double zhi) {
+    const double jmax = (1.0 + g.a1 * g.inv_R0) * (1.0 + g.a1 * g.inv_R0);
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x) {
+        unsigned long long gid = (unsigned long long)(id0 + p);
+        Philox rng;
+        rng.key = make_uint2((unsigned)seed, (unsigned)(seed >> 32));
+        rng.id_lo = (unsigned)gid;
+        rng.id_hi = (unsigned)(gid >> 32);
+        rng.draw = 0;
+        rng.used = 4;
+        double r, th;
+        for (;;) {
+            r = sqrt(g.a0 * g.a0 + (g.a1 * g.a1 - g.a0 * g.a0) * rng.u53());
+            th = GTCP_TWO_PI * rng.u53();
+            double J = 1.0 + r * g.inv_R0 * cos(th);
+            J *= J;
+            if (rng.u53() * jmax < J) break;
+        }
+        double ze = zlo + (zhi - zlo) * rng.u53();
+        if (ze >= zhi) ze = zlo;
+        double vpar;
+        do {
+            double u1 = 1.0 - rng.u53(), u2 = rng.u53();
+            vpar = sqrt(-2.0 * log(u1)) * cos(GTCP_TWO_PI * u2);
+        } while (fabs(vpar) > vcut);
+        double vperp;
+        do {
+            vperp = sqrt(-2.0 * log(1.0 - rng.u53()));
+        } while (vperp > vcut);
+        double B = 1.0 / (1.0 + r * g.inv_R0 * cos(th));
+        s.x[0][p] = 0.5 * r * r;
+        s.x[1][p] = th;
+        s.x[2][p] = ze;
+        s.x[3][p] = vpar / (g.omega0 * B);
+        s.x[4][p] = w_amp * (2.0 * rng.u53() - 1.0);
+        s.mu[p] = vperp * vperp / (2.0 * B);
+        if (s.id) s.id[p] = gid;
+    }
+}
+
+void launch_load(const Geo& g, const PSet& s, long long n, unsigned long long seed, long long id0, double w_amp,
+                 double vcut, double zlo, double zhi, cudaStream_t st) {
+    if (n <= 0) return;
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    k_load<<<blocks, 256, 0, st>>>(g, s, n, seed, id0, w_amp, vcut, zlo, zhi);
+    g_launches++;
+}
+
+}  // namespace gtcp
