@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libgtcp.so")
+LIB_PATH = os.environ.get("GTCP_LIB_PATH") or os.path.join(_HERE, "_lib", "libgtcp.so")
 
 ATTRS = ("psi", "theta", "zeta", "rho", "w", "mu", "psi0", "theta0", "zeta0", "rho0", "w0")
 GRID_CHARGE, GRID_PHI, GRID_GRADPHI, GRID_MARKER = 0, 1, 2, 3

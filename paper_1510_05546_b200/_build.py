@@ -23,8 +23,9 @@ def sources():
         [os.path.join(ROOT, "include", "gtcp.h")]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
     srcs = sources()
+    LIB = globals()["LIB"] if not debug else os.path.join(HERE, "_lib", "libgtcp_debug.so")
     if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(s) for s in srcs):
         return LIB
     inc, lib = nccl_dirs()
@@ -34,7 +35,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", inc,
            "-o", tmp] + [s for s in srcs if s.endswith(".cu")] + \
-          ["-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
+          ["-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib] + \
+          (["-DGTCP_DEBUG"] if debug else [])
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
@@ -46,4 +48,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv))

@@ -49,7 +49,7 @@ struct gtcp_ctx_s {
     Tile* tiles = nullptr;
     int max_tiles = 0;
     long long n_binned = 0;  // particles [0, n_binned) are covered by tiles
-    int tile_max = 8192;
+    int tile_max = 8192;  // <= 8192: bounds the smem limb sums (gtcp_kernels.cu smem_add)
     // grids
     long long* fx = nullptr;   // (P+1) * mgrid fixed-point charge
     double *rhoH = nullptr, *dnH = nullptr, *tmpH = nullptr, *phiH = nullptr;
@@ -296,6 +296,8 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     g.cz = p->mzetamax / GTCP_TWO_PI;
     g.dzeta = GTCP_TWO_PI / p->mzetamax;
     g.rhoG = std::sqrt(2.0) / p->omega0;
+    g.inv_omega0 = 1.0 / p->omega0;
+    g.inv_omega0_R0 = 1.0 / (p->omega0 * p->R0);
     g.mtheta = c->d_mtheta; g.igrid = c->d_igrid; g.itran = c->d_itran; g.qtinv = c->d_qtinv;
     // particle capacity: the loaded count plus headroom for shift imbalance
     long long per_plane = (long long)p->micell * (mg - M);
@@ -355,20 +357,22 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
         std::vector<double> ones(M + 1, 1.0);
         CU(cudaMemcpy(c->nm, ones.data(), sizeof(double) * (M + 1), cudaMemcpyHostToDevice));
     }
-    // tiled deposit launch configuration: 2 CTAs of 512 threads per SM
+    // tiled deposit launch configuration: 3 CTAs of 256 threads per SM
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
-    size_t table_bytes = (size_t)(P + 1) * 16 * sizeof(int);
-    size_t per_cta = std::min<size_t>((size_t)smem_optin, 110 * 1024);
+    // dynamic smem: 2 limb arrays of cap+1 words, js[(P+1) x 16] ints, column->ring bytes [cap]
+    size_t table_bytes = (size_t)(P + 1) * 16 * sizeof(int) + 64;
+    size_t per_cta = std::min<size_t>((size_t)smem_optin, 72 * 1024);
     if (per_cta < table_bytes + 8 * 1024) {
         c->dep_cap_nodes = 0;
     } else {
-        c->dep_cap_nodes = (int)((per_cta - table_bytes - 1024) / 8);
+        c->dep_cap_nodes = (int)((per_cta - table_bytes - 16) / 9);
+        c->dep_cap_nodes &= ~3;
     }
-    c->dep_smem = (size_t)c->dep_cap_nodes * 8 + table_bytes;
-    c->dep_ctas = nsm * 2;
+    c->dep_smem = (size_t)(c->dep_cap_nodes + 1) * 8 + table_bytes + c->dep_cap_nodes;
+    c->dep_ctas = nsm * 3;
     if (P + 1 > 80 || c->dep_cap_nodes < 1024) c->charge_mode = 1;
     else CU(configure_deposit_tiled(c->dep_smem));
     c->launches0 = gtcp::g_launches;
@@ -685,7 +689,7 @@ static gtcp_status do_bin(gtcp_ctx c) {
         launch_permute_u64(c->id, c->id_scratch, c->rankbuf, c->n, c->st);
         std::swap(c->id, c->id_scratch);
     }
-    launch_build_tiles(g, c->count, c->offset, c->tile_max, c->tiles, nullptr, nullptr, c->max_tiles, c->dc, c->st);
+    launch_build_tiles(g, c->offset, c->tile_max, c->tiles, c->max_tiles, c->dc, c->dep_cap_nodes, c->st);
     c->n_binned = c->n;
     KCHECK();
     return GTCP_OK;

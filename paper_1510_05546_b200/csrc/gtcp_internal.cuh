@@ -22,6 +22,7 @@ struct Geo {
     double cz;                     // mzetamax / (2 pi), rounded once (Q-2, H-1)
     double dzeta;                  // 2 pi / mzetamax
     double rhoG;                   // sqrt(2) / omega0 (F-1)
+    double inv_omega0, inv_omega0_R0;
     const int* mtheta;             // [mpsi+1]
     const int* igrid;              // [mpsi+2]
     const int* itran;              // [mpsi+1]
@@ -81,8 +82,8 @@ void launch_bin_dest(const unsigned* key, const unsigned* rank, const unsigned* 
 void launch_permute_f64(const double* src, double* dst, const unsigned* dest, long long n, cudaStream_t st);
 void launch_permute_u64(const unsigned long long* src, unsigned long long* dst, const unsigned* dest,
                         long long n, cudaStream_t st);
-void launch_build_tiles(const Geo& g, const unsigned* count, const unsigned* offset, int tile_max, Tile* tiles,
-                        int* ring_ntiles, int* ring_tile0, int max_tiles, DevCounters* dc, cudaStream_t st);
+void launch_build_tiles(const Geo& g, const unsigned* offset, int tile_max, Tile* tiles, int max_tiles,
+                        DevCounters* dc, int cap_nodes, cudaStream_t st);
 void launch_load(const Geo& g, const PSet& s, long long n, unsigned long long seed, long long id0,
                  double w_amp, double vcut, double zlo, double zhi, cudaStream_t st);
 // grid kernels (gtcp_grid.cu)

@@ -16,8 +16,16 @@
 // Paper passages: charge P:201-209; push P:224-227, P:374-378,
 // Eqs. 2-8; bin P:317-318.  Readings: SURVEY §8(c).
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "gtcp_internal.cuh"
+
+#ifdef GTCP_DEBUG
+#include <cassert>
+#define DCHECK(c) assert(c)
+#else
+#define DCHECK(c) ((void)0)
+#endif
 
 namespace gtcp {
 
@@ -25,8 +33,7 @@ long long g_launches = 0;
 
 static constexpr double kInvTwoPi = 1.0 / GTCP_TWO_PI;
 static constexpr int kMaxRings = 16;   // radial band of one tile window
-static constexpr int kDepositThreads = 512;
-static constexpr int kMaxPlanes = 80;  // P+1 planes of a tile window (host falls back to direct above)
+static constexpr int kDepositThreads = 256;
 
 // round-to-nearest-even integer of a*b for |a*b| < 2^51 (1.5*2^52 magic
 // constant, one fused rounding).  Explicit intrinsics: every kernel computes
@@ -83,13 +90,61 @@ __device__ __forceinline__ void gyro_stencil(const Geo& g, double r, double thet
     }
 }
 
+// Lane-rotated variant for the shared-memory scatter.  The 32 contributions
+// of a particle are indexed by (l, mm, kk, jj) = (point, ring, plane, node);
+// at every step lane b visits slot (l, mm, kk, jj) XOR its lane bits, so the
+// 32 lanes of a warp (cell-sorted, i.e. neighbouring particles) touch 32
+// different (point, ring, plane, node) slots instead of colliding on the same
+// shared-memory word.  Arithmetic is bit-identical to gyro_stencil.
+// fn(m, j, mt, kk, a0, a1): nodes j and j+1 (j+1 may be mt = the duplicate).
+template <class Fn>
+__device__ __forceinline__ void gyro_stencil_rot(const Geo& g, double r, double theta, double zeta, double rho,
+                                                 double inv_r, int lane, Fn&& fn) {
+    const double rho_r = __dmul_rn(rho, inv_r);
+#pragma unroll
+    for (int lq = 0; lq < 4; lq++) {
+        const int l = (lq + lane) & 3;
+        double rl = r, tl = theta;
+        if (l == 0) rl = __dadd_rn(r, rho);
+        if (l == 2) rl = __dsub_rn(r, rho);
+        if (l == 1) tl = __dadd_rn(theta, rho_r);
+        if (l == 3) tl = __dsub_rn(theta, rho_r);
+        rl = fmin(fmax(rl, g.a0), g.a1);
+        double x = __dmul_rn(__dsub_rn(rl, g.a0), g.inv_dr);
+        int i = (int)floor(x);
+        i = min(max(i, 0), g.mpsi - 1);
+        double wp1 = __dsub_rn(x, (double)i);
+#pragma unroll
+        for (int mq = 0; mq < 2; mq++) {
+            const int mm = mq ^ ((lane >> 2) & 1);
+            int m = i + mm;
+            double qt = __ldg(g.qtinv + m);
+            int mt = __ldg(g.mtheta + m);
+            double s = __dmul_rn(__fma_rn(-zeta, qt, tl), kInvTwoPi);
+            s = __dsub_rn(s, floor(s));
+            s = __dmul_rn(s, (double)mt);
+            int j = min((int)floor(s), mt - 1);
+            double wt1 = __dsub_rn(s, (double)j);
+            double wp = mm ? wp1 : __dsub_rn(1.0, wp1);
+            double a0 = __dmul_rn(__dmul_rn(0.25, wp), __dsub_rn(1.0, wt1));
+            double a1 = __dmul_rn(__dmul_rn(0.25, wp), wt1);
+#pragma unroll
+            for (int kq = 0; kq < 2; kq++) {
+                const int kk = kq ^ ((lane >> 3) & 1);
+                fn(m, j, mt, kk, a0, a1);
+            }
+        }
+    }
+}
+
 // per-particle gyroradius inputs with explicit roundings (shared by all kernels)
 __device__ __forceinline__ void gyro_radius(const Geo& g, double psi, double ct, double mu, double* r, double* invB,
                                             double* rho, double* inv_r) {
-    *r = sqrt(__dmul_rn(2.0, psi));
+    const double two_psi = __dmul_rn(2.0, psi);
+    *r = sqrt(two_psi);
+    *inv_r = rsqrt(two_psi);
     *invB = __fma_rn(__dmul_rn(*r, g.inv_R0), ct, 1.0);
-    *rho = __ddiv_rn(sqrt(__dmul_rn(__dmul_rn(2.0, mu), *invB)), g.omega0);
-    *inv_r = __drcp_rn(*r);
+    *rho = __dmul_rn(sqrt(__dmul_rn(__dmul_rn(2.0, mu), *invB)), g.inv_omega0);
 }
 
 // Global fixed-point grid index of canonical node (kk, m, j), j < mt.  On a
@@ -101,35 +156,40 @@ __device__ __forceinline__ long long fx_node(const Geo& g, int kk, int m, int j,
         j += __ldg(g.itran + m);
         j -= (j / mt) * mt;
     }
+    DCHECK(kk >= 0 && kk <= g.P && m >= 0 && m <= g.mpsi && j >= 0 && j < mt);
     return (long long)kk * g.mgrid + __ldg(g.igrid + m) + j;
 }
 
 __device__ __forceinline__ void red_i64(long long* p, long long v) {
+    DCHECK(p != nullptr);
     atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
 }
 
-// shared-memory 2-limb fixed-point add: value = hi * 2^32 + lo (carry from lo)
+// shared-memory 2-limb fixed-point add, no return value needed:
+//   v = hi * 2^17 + lo,  lo = v & (2^17 - 1) in [0, 2^17),  hi = v >> 17.
+// With |v| < 2^33 and at most 4 * kTileMax = 2^15 contributions per node per
+// tile, sum(lo) < 2^32 and |sum(hi)| < 2^31: both limbs are exact (native
+// 32-bit ATOMS.ADD, 24 lane-ops/SM/clk measured on B200).
+static constexpr int kLimbBits = 17;
 __device__ __forceinline__ void smem_add(unsigned* lo, int* hi, int slot, long long v) {
-    unsigned vlo = (unsigned)v;
-    int vhi = (int)(v >> 32);
-    unsigned old = atomicAdd(lo + slot, vlo);
-    vhi += (old + vlo < old) ? 1 : 0;
-    if (vhi) atomicAdd(hi + slot, vhi);
+    atomicAdd(lo + slot, (unsigned)v & ((1u << kLimbBits) - 1u));
+    atomicAdd(hi + slot, (int)(v >> kLimbBits));
 }
 
 __device__ __forceinline__ double fx_scale(const DevCounters* dc) { return scalbn(1.0, dc->fx_shift); }
 
 // ---------------------------------------------------------------------------
-// charge: fixed-point scale.  F = 42 - ceil(log2 max|w|) so |w| 2^F <= 2^42 and
-// every contribution (<= |w|/4) rounds to an integer below 2^40.
+// charge: fixed-point scale.  F = 35 - e with max|w| in [2^(e-1), 2^e), so
+// |w| 2^F < 2^35 and every contribution (<= |w|/4) rounds to an integer of
+// magnitude below 2^33 (33-bit contributions; precision analysis DESIGN.md §5).
 // ---------------------------------------------------------------------------
 __global__ void k_fx_scale(DevCounters* dc) {
     double wmax = __longlong_as_double((long long)dc->wmax_bits);
-    int F = 42;
+    int F = 35;
     if (wmax > 0.0 && isfinite(wmax)) {
         int e;
         frexp(wmax, &e);  // wmax in [2^(e-1), 2^e)
-        F = 42 - e;
+        F = 35 - e;
     }
     F = max(-60, min(F, 60));
     dc->fx_shift = F;
@@ -187,25 +247,82 @@ void launch_deposit_direct(const Geo& g, const PSet& s, long long begin, long lo
 // ---------------------------------------------------------------------------
 // charge: tiled deposit.
 // ---------------------------------------------------------------------------
+// Tile window (all local planes x rings m_lo..m_hi x a label window per ring):
+// ring halo h from the gyroradius cutoff; label half-width on ring m =
+// tile half-width + field-line skew over +-dzeta + theta-point margin (rings
+// i-1..i+2) + one cell of drift since the bin.
+__device__ __forceinline__ int win_halo(const Geo& g, double rho_cut) {
+    int h = (int)ceil(rho_cut * g.inv_dr) + 1;
+    return min(h, (kMaxRings - 2) / 2);
+}
+
+__device__ __forceinline__ double win_halfwidth(const Geo& g, int i, int c0, int c1, int m, double rho_cut,
+                                                double* dq_out) {
+    int mti = __ldg(g.mtheta + i);
+    double half0 = 0.5 * (double)(c1 + 1 - c0) / mti;
+    double dq = (__ldg(g.qtinv + i) - __ldg(g.qtinv + m)) * kInvTwoPi;
+    double rm = g.a0 + m * g.dr;
+    double thm = (m >= i - 1 && m <= i + 2) ? rho_cut / rm * kInvTwoPi : 0.0;
+    *dq_out = dq;
+    return half0 + g.dzeta * fabs(dq) + thm + 1.0 / __ldg(g.mtheta + m);
+}
+
+__device__ __forceinline__ int win_width(const Geo& g, int i, int c0, int c1, int m, double rho_cut) {
+    double dq;
+    double hw = win_halfwidth(g, i, c0, c1, m, rho_cut, &dq);
+    int mt = __ldg(g.mtheta + m);
+    return min((int)ceil(2.0 * hw * mt) + 2, mt);
+}
+
+__device__ __forceinline__ int win_nodes(const Geo& g, int i, int c0, int c1, double rho_cut) {
+    int h = win_halo(g, rho_cut);
+    int m_lo = max(0, i - h), m_hi = min(g.mpsi, i + 1 + h);
+    int S = 0;
+    for (int m = m_lo; m <= m_hi; m++) S += win_width(g, i, c0, c1, m, rho_cut);
+    return S * (g.P + 1);
+}
+
+static double deposit_rho_cut(const Geo& g) { return 3.0 / g.omega0; }
+
 struct WinTables {
     int m_lo, nr, S, total;
-    int W[kMaxRings], off[kMaxRings], mt[kMaxRings];
+    int2 WO[kMaxRings];  // (window width W, column offset) per ring of the band
+    int mt[kMaxRings];
     long long start, end;
     int tile;
 };
 
-__global__ void __launch_bounds__(kDepositThreads, 2)
+// limbs of the fixed-point value v = round(a*b) taken straight from the bits of
+// t = fma(a, b, 1.5*2^52): the low 17 bits of v are the low 17 bits of t, and
+// v >> 17 (|v| < 2^33) is bits 17..48 of t read as a signed int (the 2^51
+// offset of the magic constant vanishes mod 2^32).
+__device__ __forceinline__ double fx_magic(double a, double b) { return __fma_rn(a, b, 6755399441055744.0); }
+__device__ __forceinline__ unsigned fx_lo(double t) { return (unsigned)__double2loint(t) & ((1u << kLimbBits) - 1u); }
+__device__ __forceinline__ int fx_hi(double t) {
+    return (int)__funnelshift_r((unsigned)__double2loint(t), (unsigned)__double2hiint(t), kLimbBits);
+}
+__device__ __forceinline__ long long fx_val(double t) {
+    return __double_as_longlong(t) - __double_as_longlong(6755399441055744.0);
+}
+
+__global__ void __launch_bounds__(kDepositThreads, 3)
     k_deposit_tiled(Geo g, PSet s, long long n, const Tile* __restrict__ tiles, const int* ntiles_p,
                     long long* __restrict__ fx, DevCounters* dc, int cap_nodes, double rho_cut) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    // limbs: cap_nodes + 1 words each (the last one is a trash slot for
+    // contributions outside the window, which go to L2 instead)
     unsigned* slo = reinterpret_cast<unsigned*>(smem_raw);
-    int* shi = reinterpret_cast<int*>(slo + cap_nodes);
-    int* js = shi + cap_nodes;  // [(P+1) * nr]
+    int* shi = reinterpret_cast<int*>(slo + cap_nodes + 1);
+    int* js = shi + cap_nodes + 1;             // [(P+1) * nr] window start per (plane, ring)
+    unsigned char* colq = reinterpret_cast<unsigned char*>(js + (g.P + 1) * kMaxRings);  // [S] ring of column
     __shared__ WinTables T;
     __shared__ unsigned long long s_fallback;
     const double scale = fx_scale(dc);
     const int ntiles = *ntiles_p;
     const int P1 = g.P + 1;
+    const int trash = cap_nodes;
+    const int lane = threadIdx.x & 31;
+    const int b2 = (lane >> 2) & 1, b3 = (lane >> 3) & 1, b4 = (lane >> 4) & 1;
     if (threadIdx.x == 0) s_fallback = 0;
 
     for (;;) {
@@ -213,127 +330,174 @@ __global__ void __launch_bounds__(kDepositThreads, 2)
         __syncthreads();
         const int t = T.tile;
         if (t >= ntiles) break;
-        // ---- window of this tile (rings m_lo..m_lo+nr-1, label window per ring/plane)
+        const Tile tl = tiles[t];
+        // ---- window of this tile: rings m_lo..m_lo+nr-1, a label window per (plane, ring)
         if (threadIdx.x == 0) {
-            Tile tl = tiles[t];
             int i = tl.ring;
-            int h = (int)ceil(rho_cut * g.inv_dr) + 1;
-            h = min(h, (kMaxRings - 2) / 2);
+            int h = win_halo(g, rho_cut);
             int m_lo = max(0, i - h), m_hi = min(g.mpsi, i + 1 + h);
             T.m_lo = m_lo;
             T.nr = m_hi - m_lo + 1;
             T.start = tl.start;
             T.end = min(tl.end, n);
             int S = 0;
-            int mti = __ldg(g.mtheta + i);
-            double half0 = 0.5 * (double)(tl.c1 + 1 - tl.c0) / mti;
-            double qti = __ldg(g.qtinv + i);
             for (int q = 0; q < T.nr; q++) {
                 int m = m_lo + q;
-                int mt = __ldg(g.mtheta + m);
-                double dq = (qti - __ldg(g.qtinv + m)) * kInvTwoPi;
-                double rm = g.a0 + m * g.dr;
-                double thm = (m >= i - 1 && m <= i + 2) ? rho_cut / rm * kInvTwoPi : 0.0;
-                double hw = half0 + g.dzeta * fabs(dq) + thm + 1.0 / mt;
-                int W = (int)ceil(2.0 * hw * mt) + 2;
-                W = min(W, mt);
-                T.W[q] = W;
-                T.mt[q] = mt;
-                T.off[q] = S;
+                int W = win_width(g, i, tl.c0, tl.c1, m, rho_cut);
+                T.WO[q] = make_int2(W, S);
+                T.mt[q] = __ldg(g.mtheta + m);
                 S += W;
             }
             T.S = S;
             T.total = S * P1;
-            if (T.total > cap_nodes) {  // pathological window: everything via L2
+            if (T.total > cap_nodes) {  // window too large for shared memory: everything via L2
                 T.total = 0;
-                for (int q = 0; q < T.nr; q++) T.W[q] = 0;
+                T.S = 0;
+                for (int q = 0; q < T.nr; q++) T.WO[q] = make_int2(0, 0);
             }
+            for (int q = T.nr; q < kMaxRings; q++) T.WO[q] = make_int2(0, 0);
         }
         __syncthreads();
         {
-            Tile tl = tiles[t];
-            int i = tl.ring;
-            int mti = __ldg(g.mtheta + i);
-            double fc = 0.5 * (double)(tl.c0 + tl.c1 + 1) / mti;
-            double half0 = 0.5 * (double)(tl.c1 + 1 - tl.c0) / mti;
-            double qti = __ldg(g.qtinv + i);
+            const int i = tl.ring;
+            const int mti = __ldg(g.mtheta + i);
+            const double fc = 0.5 * (double)(tl.c0 + tl.c1 + 1) / mti;
             for (int e = threadIdx.x; e < P1 * T.nr; e += blockDim.x) {
                 int kk = e / T.nr, q = e - kk * T.nr;
                 int m = T.m_lo + q;
                 int mt = T.mt[q];
-                double dq = (qti - __ldg(g.qtinv + m)) * kInvTwoPi;
-                double rm = g.a0 + m * g.dr;
-                double thm = (m >= i - 1 && m <= i + 2) ? rho_cut / rm * kInvTwoPi : 0.0;
-                double hw = half0 + g.dzeta * fabs(dq) + thm + 1.0 / mt;
+                double dq;
+                double hw = win_halfwidth(g, i, tl.c0, tl.c1, m, rho_cut, &dq);
                 double zk = (double)(g.k0 + kk) * g.dzeta;
                 double f = fc + zk * dq - hw;
                 f = f - floor(f);
-                int j0 = (int)floor(f * mt);
-                j0 = min(max(j0, 0), mt - 1);
-                js[e] = j0;
+                DCHECK(kk * kMaxRings + q < P1 * kMaxRings);
+                js[kk * kMaxRings + q] = min(max((int)floor(f * mt), 0), mt - 1);
             }
-            for (int e = threadIdx.x; e < T.total; e += blockDim.x) {
-                slo[e] = 0u;
-                shi[e] = 0;
+            for (int q = 0; q < T.nr; q++)
+                for (int x = threadIdx.x; x < T.WO[q].x; x += blockDim.x) colq[T.WO[q].y + x] = (unsigned char)q;
+            uint4* z4 = reinterpret_cast<uint4*>(slo);
+            const int nz = (2 * (cap_nodes + 1)) / 4;  // both limb arrays are contiguous
+            const int nzt = (2 * T.total + 3) / 4;
+            (void)nz;
+            // zero the used part of both limb arrays (they are not contiguous over total; do each)
+            for (int e = threadIdx.x; e < (T.total + 3) / 4; e += blockDim.x) {
+                if (4 * e + 3 < T.total) {
+                    z4[e] = make_uint4(0, 0, 0, 0);
+                } else {
+                    for (int u = 4 * e; u < T.total; u++) slo[u] = 0u;
+                }
             }
+            for (int e = threadIdx.x; e < T.total; e += blockDim.x) shi[e] = 0;
+            (void)nzt;
         }
         __syncthreads();
-        // ---- deposit the tile's particles
+        // ---- deposit the tile's particles (Q-1..Q-6)
         const int m_lo = T.m_lo, nr = T.nr, S = T.S;
         unsigned long long fb = 0;
         long long clamps = 0;
         for (long long p = T.start + threadIdx.x; p < T.end; p += blockDim.x) {
-            double psi = s.x[0][p], theta = s.x[1][p], zeta = s.x[2][p], w = s.x[4][p], mu = s.mu[p];
+            const double psi = s.x[0][p], theta = s.x[1][p], zeta = s.x[2][p], w = s.x[4][p], mu = s.mu[p];
             double r, invB, rho, inv_r;
             gyro_radius(g, psi, cos(theta), mu, &r, &invB, &rho, &inv_r);
             double wz1;
-            int kg = plane_of(g, zeta, &wz1);
+            const int kg = plane_of(g, zeta, &wz1);
             int k = kg - g.k0;
             if (k < 0 || k > g.P - 1) { clamps++; k = min(max(k, 0), g.P - 1); }
-            double ws = __dmul_rn(w, scale);
-            double wz[2] = {__dmul_rn(__dsub_rn(1.0, wz1), ws), __dmul_rn(wz1, ws)};
-            gyro_stencil(g, r, theta, zeta, rho, inv_r, [&](int m, int j, int mt, double a0, double a1) {
-                int j1 = (j + 1 == mt) ? 0 : j + 1;
-                int q = m - m_lo;
-                bool inr = (unsigned)q < (unsigned)nr;
+            const double ws = __dmul_rn(w, scale);
+            const double wzl = __dmul_rn(__dsub_rn(1.0, wz1), ws), wzu = __dmul_rn(wz1, ws);
+            const double rho_r = __dmul_rn(rho, inv_r);
 #pragma unroll
-                for (int kk = 0; kk < 2; kk++) {
-                    long long v0 = fx_round(wz[kk], a0), v1 = fx_round(wz[kk], a1);
-                    int d = -1, d1 = -1, W = 0, base = 0;
-                    if (inr) {
-                        W = T.W[q];
-                        base = (k + kk) * S + T.off[q];
-                        d = j - js[(k + kk) * nr + q];
-                        if (d < 0) d += mt;
-                        d1 = (d + 1 == mt) ? 0 : d + 1;
-                    }
-                    if (v0) {
-                        if (inr && d < W) smem_add(slo, shi, base + d, v0);
-                        else { red_i64(fx + fx_node(g, k + kk, m, j, mt), v0); fb++; }
-                    }
-                    if (v1) {
-                        if (inr && d1 < W) smem_add(slo, shi, base + d1, v1);
-                        else { red_i64(fx + fx_node(g, k + kk, m, j1, mt), v1); fb++; }
+            for (int l = 0; l < 4; l++) {
+                double rl = r, tl2 = theta;
+                if (l == 0) rl = __dadd_rn(r, rho);
+                if (l == 2) rl = __dsub_rn(r, rho);
+                if (l == 1) tl2 = __dadd_rn(theta, rho_r);
+                if (l == 3) tl2 = __dsub_rn(theta, rho_r);
+                rl = fmin(fmax(rl, g.a0), g.a1);
+                const double x = __dmul_rn(__dsub_rn(rl, g.a0), g.inv_dr);
+                const int ir = min(max((int)floor(x), 0), g.mpsi - 1);
+                const double wp1 = __dsub_rn(x, (double)ir);
+#pragma unroll
+                for (int mq = 0; mq < 2; mq++) {
+                    const int mm = mq ^ b2;  // lane-rotated ring choice
+                    const int m = ir + mm;
+                    const double qt = __ldg(g.qtinv + m);
+                    const int mt = __ldg(g.mtheta + m);
+                    double sl = __dmul_rn(__fma_rn(-zeta, qt, tl2), kInvTwoPi);
+                    sl = __dsub_rn(sl, floor(sl));
+                    sl = __dmul_rn(sl, (double)mt);
+                    const int j = min((int)floor(sl), mt - 1);
+                    const double wt1 = __dsub_rn(sl, (double)j);
+                    const double wp = mm ? wp1 : __dsub_rn(1.0, wp1);
+                    const double a0 = __dmul_rn(__dmul_rn(0.25, wp), __dsub_rn(1.0, wt1));
+                    const double a1 = __dmul_rn(__dmul_rn(0.25, wp), wt1);
+                    const int q = m - m_lo;
+                    const bool inr = (unsigned)q < (unsigned)nr;
+                    const int qc = inr ? q : 0;
+                    const int2 wo = T.WO[qc];
+                    const int W = inr ? wo.x : 0;
+                    const int j1 = (j + 1 == mt) ? 0 : j + 1;
+                    // node order j / j+1 rotated by lane bit 4
+                    const int ja = b4 ? j1 : j, jb = b4 ? j : j1;
+                    const double aa = b4 ? a1 : a0, ab = b4 ? a0 : a1;
+#pragma unroll
+                    for (int kq = 0; kq < 2; kq++) {
+                        const int kk = kq ^ b3;  // lane-rotated plane choice
+                        const int kp = k + kk;
+                        const double wzk = kk ? wzu : wzl;
+                        int d = j - js[kp * kMaxRings + qc];
+                        d += (d < 0) ? mt : 0;
+                        d = inr ? d : 0;  // outside the band: js belongs to another ring (W = 0 anyway)
+                        const int d1 = (d + 1 == mt) ? 0 : d + 1;
+                        const int da = b4 ? d1 : d, db = b4 ? d : d1;
+                        const double ta = fx_magic(wzk, aa), tb = fx_magic(wzk, ab);
+                        const bool oka = da < W, okb = db < W;
+                        const int base = kp * S + wo.y;
+                        const int sa = oka ? base + da : trash, sb = okb ? base + db : trash;
+#ifdef GTCP_DEBUG
+                        if (!(sa >= 0 && sa <= trash && sb >= 0 && sb <= trash))
+                            printf("BAD slot sa=%d sb=%d da=%d db=%d d=%d j=%d mt=%d js=%d W=%d base=%d kp=%d q=%d nr=%d S=%d "
+                                   "total=%d cap=%d m=%d mlo=%d sl=%g zeta=%g theta=%g psi=%g tile=%d\n",
+                                   sa, sb, da, db, d, j, mt, js[kp * kMaxRings + qc], W, base, kp, q, nr, S, T.total,
+                                   cap_nodes, m, m_lo, sl, zeta, theta, psi, t);
+#endif
+                        DCHECK(sa >= 0 && sa <= trash && sb >= 0 && sb <= trash);
+                        DCHECK(kp * kMaxRings + qc < P1 * kMaxRings && kp >= 0);
+                        atomicAdd(slo + sa, fx_lo(ta));
+                        atomicAdd(shi + sa, fx_hi(ta));
+                        atomicAdd(slo + sb, fx_lo(tb));
+                        atomicAdd(shi + sb, fx_hi(tb));
+                        if (__builtin_expect(!(oka && okb), 0)) {
+                            if (!oka) { long long v = fx_val(ta); if (v) { red_i64(fx + fx_node(g, kp, m, ja, mt), v); fb++; } }
+                            if (!okb) { long long v = fx_val(tb); if (v) { red_i64(fx + fx_node(g, kp, m, jb, mt), v); fb++; } }
+                        }
                     }
                 }
-            });
+            }
         }
         if (fb) atomicAdd(&s_fallback, fb);
         if (clamps) atomicAdd((unsigned long long*)&dc->plane_clamps, (unsigned long long)clamps);
         __syncthreads();
         // ---- flush the window to L2 (one REDG.ADD.64 per nonzero node)
-        for (int e = threadIdx.x; e < T.total; e += blockDim.x) {
-            long long v = (long long)(((unsigned long long)(unsigned)shi[e] << 32) + (unsigned long long)slo[e]);
-            if (v == 0) continue;
-            int kk = e / S;
-            int rem = e - kk * S;
-            int q = 0;
-            while (q + 1 < nr && T.off[q + 1] <= rem) q++;
-            int d = rem - T.off[q];
-            int mt = T.mt[q];
-            int j = js[kk * nr + q] + d;
-            if (j >= mt) j -= mt;
-            red_i64(fx + fx_node(g, kk, m_lo + q, j, mt), v);
+        if (S > 0) {
+            int kk = threadIdx.x / S, x = threadIdx.x - kk * S;
+            const int bdiv = blockDim.x / S, bmod = blockDim.x - bdiv * S;
+            for (int e = threadIdx.x; e < T.total; e += blockDim.x) {
+                long long v = (long long)shi[e] * (1LL << kLimbBits) + (long long)slo[e];
+                if (v != 0) {
+                    DCHECK(x >= 0 && x < S && kk >= 0 && kk < P1);
+                    const int q = colq[x];
+                    DCHECK(q < nr);
+                    const int mt = T.mt[q];
+                    int j = js[kk * kMaxRings + q] + (x - T.WO[q].y);
+                    if (j >= mt) j -= mt;
+                    red_i64(fx + fx_node(g, kk, m_lo + q, j, mt), v);
+                }
+                x += bmod;
+                kk += bdiv;
+                if (x >= S) { x -= S; kk++; }
+            }
         }
         __syncthreads();
     }
@@ -348,7 +512,7 @@ void launch_deposit_tiled(const Geo& g, const PSet& s, long long n, const Tile* 
                           long long* fx, DevCounters* dc, int ctas, size_t smem_bytes, int cap_nodes,
                           cudaStream_t st) {
     (void)max_tiles;
-    double rho_cut = 3.0 / g.omega0;
+    double rho_cut = deposit_rho_cut(g);
     k_deposit_tiled<<<ctas, kDepositThreads, smem_bytes, st>>>(g, s, n, tiles, &dc->ntiles, fx, dc, cap_nodes,
                                                               rho_cut);
     g_launches++;
@@ -391,7 +555,8 @@ __device__ __forceinline__ double warp_max(double v) {
     return v;
 }
 
-__global__ void __launch_bounds__(256) k_push(Geo g, PushPtrs pp, long long n, double h,
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long long n, double h,
                                              const double* __restrict__ gf, DevCounters* dc) {
     double wmax = 0.0;
     long long refl = 0, clamps = 0;
@@ -406,7 +571,10 @@ __global__ void __launch_bounds__(256) k_push(Geo g, PushPtrs pp, long long n, d
         double r, invB, rho, inv_r;
         gyro_radius(g, psi, ct, mu, &r, &invB, &rho, &inv_r);
         const double eps = r * g.inv_R0;
-        const double B = 1.0 / invB;
+        const double q = g.q0 + g.q2 * r * r;
+        const double inv_qB = 1.0 / (q * invB);  // one division: 1/q and B follow
+        const double B = q * inv_qB;
+        const double inv_q = invB * inv_qB;
         // U-2 gather
         double wz1;
         int kg = plane_of(g, zeta, &wz1);
@@ -416,9 +584,9 @@ __global__ void __launch_bounds__(256) k_push(Geo g, PushPtrs pp, long long n, d
         double gr = 0.0, gt = 0.0, gp = 0.0;
         const double* gk = gf + (long long)k * g.mgrid * 6;
         gyro_stencil(g, r, theta, zeta, rho, inv_r, [&](int m, int j, int mt, double a0, double a1) {
-            const double2* q = reinterpret_cast<const double2*>(gk + ((long long)__ldg(g.igrid + m) + j) * 6);
-            double2 v0 = __ldg(q + 0), v1 = __ldg(q + 1), v2 = __ldg(q + 2);
-            double2 v3 = __ldg(q + 3), v4 = __ldg(q + 4), v5 = __ldg(q + 5);
+            const double2* qq = reinterpret_cast<const double2*>(gk + ((long long)__ldg(g.igrid + m) + j) * 6);
+            double2 v0 = __ldg(qq + 0), v1 = __ldg(qq + 1), v2 = __ldg(qq + 2);
+            double2 v3 = __ldg(qq + 3), v4 = __ldg(qq + 4), v5 = __ldg(qq + 5);
             // node j: (v0.x v0.y v1.x) plane k, (v1.y v2.x v2.y) plane k+1; node j+1 likewise in v3..v5
             double c00 = a0 * wz0, c01 = a0 * wz1, c10 = a1 * wz0, c11 = a1 * wz1;
             gr += c00 * v0.x + c01 * v1.y + c10 * v3.x + c11 * v4.y;
@@ -427,32 +595,32 @@ __global__ void __launch_bounds__(256) k_push(Geo g, PushPtrs pp, long long n, d
             (void)mt;
         });
         // U-3 drifts
-        const double q = g.q0 + g.q2 * r * r;
         const double vpar = g.omega0 * B * rho_par;
+        const double iOB = g.inv_omega0 * invB;  // 1 / (omega0 B)
         double vEr = 0.0, vEt = 0.0, vdr = 0.0, vdt = 0.0;
         if (g.drifts) {
-            vEr = -gt * inv_r / (g.omega0 * B);
-            vEt = gr / (g.omega0 * B);
-            const double Cd = (vpar * vpar + mu * B) / (g.omega0 * g.R0);
+            vEr = -gt * inv_r * iOB;
+            vEt = gr * iOB;
+            const double Cd = (vpar * vpar + mu * B) * g.inv_omega0_R0;
             vdr = -Cd * st;
             vdt = -Cd * ct;
         }
         // U-4
         const double rdot = vEr + vdr;
         const double psidot = r * rdot;
-        const double thdot = vpar * B / (q * g.R0) + (vEt + vdt) * inv_r;
+        const double thdot = vpar * B * inv_q * g.inv_R0 + (vEt + vdt) * inv_r;
         const double zdot = vpar * B * g.inv_R0;
         // U-5
-        double vdot = -mu * B * B * B * r * st / (q * g.R0 * g.R0);
+        double vdot = -mu * B * B * B * r * st * inv_q * g.inv_R0 * g.inv_R0;
         if (g.paranl) {
             double par = -(B * g.inv_R0) * gp;
-            if (g.drifts) par += (vpar / (g.omega0 * g.R0)) * (st * gr + ct * gt * inv_r);
+            if (g.drifts) par += vpar * g.inv_omega0_R0 * (st * gr + ct * gt * inv_r);
             vdot += par;
         }
         const double dBdr = -B * B * ct * g.inv_R0;
         const double dBdt = B * B * eps * st;
         const double Bdot = rdot * dBdr + thdot * dBdt;
-        const double rhodot = (vdot - vpar * Bdot * invB) / (g.omega0 * B);
+        const double rhodot = (vdot - vpar * Bdot * invB) * iOB;
         // U-6 delta-f weight
         const double Ekin = 0.5 * vpar * vpar + mu * B;
         const double x6 = (r - 0.5) * (1.0 / 0.35);
@@ -469,9 +637,12 @@ __global__ void __launch_bounds__(256) k_push(Geo g, PushPtrs pp, long long n, d
         // U-8 wrap angles (same operation sequence as the oracle) and reflect r
 #pragma unroll
         for (int d = 1; d <= 2; d++) {
-            double t = __dsub_rn(X[d], __dmul_rn(GTCP_TWO_PI, floor(__ddiv_rn(X[d], GTCP_TWO_PI))));
-            if (t >= GTCP_TWO_PI) t = 0.0;
-            X[d] = t;
+            // X in [0, 2 pi): floor(X / 2 pi) = 0 and the oracle's expression returns X itself
+            if (X[d] < 0.0 || X[d] >= GTCP_TWO_PI) {
+                double t = __dsub_rn(X[d], __dmul_rn(GTCP_TWO_PI, floor(__ddiv_rn(X[d], GTCP_TWO_PI))));
+                if (t >= GTCP_TWO_PI) t = 0.0;
+                X[d] = t;
+            }
         }
         double rn = sqrt(2.0 * fmax(X[0], 0.0));
         bool rf = false;
@@ -503,7 +674,13 @@ void launch_push3(const Geo& g, const double* const src[5], const double* const 
     }
     pp.mu = mu;
     int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
-    k_push<<<blocks, 256, 0, st>>>(g, pp, n, h, gfield, dc);
+    static int minb = [] {
+        const char* e = getenv("GTCP_PUSH_MINB");
+        return e ? atoi(e) : 2;
+    }();
+    if (minb == 3) k_push<3><<<blocks, 256, 0, st>>>(g, pp, n, h, gfield, dc);
+    else if (minb == 1) k_push<1><<<blocks, 256, 0, st>>>(g, pp, n, h, gfield, dc);
+    else k_push<2><<<blocks, 256, 0, st>>>(g, pp, n, h, gfield, dc);
     g_launches++;
 }
 
@@ -693,7 +870,7 @@ void launch_permute_u64(const unsigned long long* src, unsigned long long* dst, 
 // offsets: cell c of ring i owns keys [(igrid_i+c)P, (igrid_i+c+1)P)) and
 // greedily packs consecutive cells into tiles of at most tile_max particles.
 __device__ __forceinline__ int ring_tiles(const Geo& g, int i, const unsigned* offset, int tile_max,
-                                          Tile* out, int max_out) {
+                                          Tile* out, int max_out, int cap_nodes, double rho_cut) {
     int mt = __ldg(g.mtheta + i), ig = __ldg(g.igrid + i);
     int nt = 0;
     long long cur = 0, tstart = offset[(long long)ig * g.P];
@@ -712,7 +889,7 @@ __device__ __forceinline__ int ring_tiles(const Geo& g, int i, const unsigned* o
         long long ce = offset[(long long)(ig + c + 1) * g.P];
         long long cnt = ce - cs;
         if (cnt == 0) continue;
-        if (cur > 0 && cur + cnt > tile_max) {
+        if (cur > 0 && (cur + cnt > tile_max || win_nodes(g, i, c0, c, rho_cut) > cap_nodes)) {
             emit(c0, c - 1 < c0 ? c0 : c - 1, tstart, cs);
             cur = 0;
             tstart = cs;
@@ -732,7 +909,8 @@ __device__ __forceinline__ int ring_tiles(const Geo& g, int i, const unsigned* o
 }
 
 __global__ void __launch_bounds__(1024) k_build_tiles(Geo g, const unsigned* __restrict__ offset, int tile_max,
-                                                      Tile* tiles, int max_tiles, DevCounters* dc) {
+                                                      Tile* tiles, int max_tiles, DevCounters* dc, int cap_nodes,
+                                                      double rho_cut) {
     __shared__ unsigned sm[32];
     __shared__ unsigned s_carry;
     if (threadIdx.x == 0) s_carry = 0;
@@ -740,12 +918,12 @@ __global__ void __launch_bounds__(1024) k_build_tiles(Geo g, const unsigned* __r
     // rings with gyrocentres: 0..mpsi-1 (bin key uses the floor ring)
     for (int b0 = 0; b0 < g.mpsi; b0 += 1024) {
         int i = b0 + threadIdx.x;
-        unsigned cnt = (i < g.mpsi) ? (unsigned)ring_tiles(g, i, offset, tile_max, nullptr, 0) : 0u;
+        unsigned cnt = (i < g.mpsi) ? (unsigned)ring_tiles(g, i, offset, tile_max, nullptr, 0, cap_nodes, rho_cut) : 0u;
         unsigned tot;
         unsigned ex = block_exclusive_scan(cnt, sm, &tot) + s_carry;
         if (i < g.mpsi) {
             int room = max_tiles - (int)ex;
-            if (room > 0) ring_tiles(g, i, offset, tile_max, tiles + ex, room);
+            if (room > 0) ring_tiles(g, i, offset, tile_max, tiles + ex, room, cap_nodes, rho_cut);
         }
         __syncthreads();
         if (threadIdx.x == 0) s_carry += tot;
@@ -754,10 +932,9 @@ __global__ void __launch_bounds__(1024) k_build_tiles(Geo g, const unsigned* __r
     if (threadIdx.x == 0) dc->ntiles = min((int)s_carry, max_tiles);
 }
 
-void launch_build_tiles(const Geo& g, const unsigned* count, const unsigned* offset, int tile_max, Tile* tiles,
-                        int* ring_ntiles, int* ring_tile0, int max_tiles, DevCounters* dc, cudaStream_t st) {
-    (void)count; (void)ring_ntiles; (void)ring_tile0;
-    k_build_tiles<<<1, 1024, 0, st>>>(g, offset, tile_max, tiles, max_tiles, dc);
+void launch_build_tiles(const Geo& g, const unsigned* offset, int tile_max, Tile* tiles, int max_tiles,
+                        DevCounters* dc, int cap_nodes, cudaStream_t st) {
+    k_build_tiles<<<1, 1024, 0, st>>>(g, offset, tile_max, tiles, max_tiles, dc, cap_nodes, deposit_rho_cut(g));
     g_launches++;
 }
 

@@ -70,7 +70,7 @@ def test_charge_parity_T(G, orc, T, mode):
     ref = orc.charge_global(p, parts)
     assert got.shape == ref.shape
     assert rel_err(got, ref) <= TOL
-    assert rel_err(got, ref) <= 1e-10  # fixed-point sums: far inside TOL
+    assert rel_err(got, ref) <= 1e-8  # 33-bit fixed-point contributions: far inside TOL
 
 
 def test_charge_tiled_equals_direct_bitwise(G, T):
@@ -96,7 +96,7 @@ def test_charge_parity_A_grid(G, orc):
     ctx.charge()
     got = ctx.get_grid(G.GRID_CHARGE)
     ref = orc.charge_global(p, parts)
-    assert rel_err(got, ref) <= 1e-10
+    assert rel_err(got, ref) <= 1e-8
     st = ctx.stats()
     assert st["plane_clamps"] == 0
 
@@ -105,7 +105,7 @@ def test_marker_norm_parity(G, orc, T):
     cfg, p, g, parts = T
     ctx = ctx_for(G, "T")
     ctx.set_particles(parts)
-    assert rel_err(ctx.get_grid(G.GRID_MARKER), orc.marker_norm(p, parts)) <= 1e-12
+    assert rel_err(ctx.get_grid(G.GRID_MARKER), orc.marker_norm(p, parts)) <= 1e-8
 
 
 # ------------------------------------------------------------------ grid kernels
