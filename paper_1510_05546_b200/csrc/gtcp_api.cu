@@ -73,7 +73,11 @@ struct gtcp_ctx_s {
     double* recvR[12] = {};
     unsigned long long *sidL = nullptr, *sidR = nullptr, *ridL = nullptr, *ridR = nullptr;
     unsigned char* cls = nullptr;
-    unsigned* bcount = nullptr;  // per-block counts (3 per block) + scan
+    unsigned* bcount = nullptr;  // per-block counts and offsets (8 arrays of shift_blocks+1)
+    unsigned* holes = nullptr;   // hole positions, shift_cap
+    long long* d_nkeep = nullptr;
+    long long* d_counts = nullptr;  // [myL, myR, fromRight, fromLeft, mine, total]
+    long long* h_counts = nullptr;  // pinned mirror
     int shift_blocks = 0;
     long long movers_sent = 0, movers_recv = 0;
     // charge config
@@ -390,18 +394,23 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
         for (int d = 0; d < 11; d++) {
             CU(dalloc(&c->sendL[d], c->shift_cap));
             CU(dalloc(&c->sendR[d], c->shift_cap));
-            CU(dalloc(&c->recvL[d], c->shift_cap));
-            CU(dalloc(&c->recvR[d], c->shift_cap));
         }
         if (p->track_ids) {
             CU(dalloc(&c->sidL, c->shift_cap));
             CU(dalloc(&c->sidR, c->shift_cap));
-            CU(dalloc(&c->ridL, c->shift_cap));
-            CU(dalloc(&c->ridR, c->shift_cap));
         }
         CU(dalloc(&c->cls, c->cap));
         c->shift_blocks = (int)((c->cap + 1023) / 1024);
-        CU(dalloc(&c->bcount, 3LL * (c->shift_blocks + 1) * 2));
+        CU(dalloc(&c->bcount, 8LL * (c->shift_blocks + 1)));
+        CU(dalloc(&c->holes, c->shift_cap));
+        CU(dalloc(&c->d_nkeep, 1));
+        CU(dalloc(&c->d_counts, 8));
+        CU(cudaMallocHost((void**)&c->h_counts, 8 * sizeof(long long)));
+        // scan scratch must cover the per-block count arrays too
+        if ((c->shift_blocks + 4095) / 4096 + 1 > (c->nkeys + 4095) / 4096 + 1) {
+            cudaFree(c->scan_tmp);
+            CU(dalloc(&c->scan_tmp, (c->shift_blocks + 4095) / 4096 + 1));
+        }
     }
     CU(cudaDeviceSynchronize());
     return GTCP_OK;
@@ -420,7 +429,9 @@ extern "C" void gtcp_destroy(gtcp_ctx c) {
     F(c->gfield); F(c->nm); F(c->ringsum); F(c->phi00); F(c->halo_buf); F(c->fx_recv); F(c->dc); F(c->d_scalar); F(c->d_partial);
     F(c->d_mtheta); F(c->d_igrid); F(c->d_itran); F(c->d_qtinv);
     for (int d = 0; d < 12; d++) { F(c->sendL[d]); F(c->sendR[d]); F(c->recvL[d]); F(c->recvR[d]); }
-    F(c->sidL); F(c->sidR); F(c->ridL); F(c->ridR); F(c->cls); F(c->bcount);
+    F(c->sidL); F(c->sidR); F(c->ridL); F(c->ridR); F(c->cls); F(c->bcount); F(c->holes); F(c->d_nkeep);
+    F(c->d_counts);
+    if (c->h_counts) cudaFreeHost(c->h_counts);
     if (c->h_dc) cudaFreeHost(c->h_dc);
     if (c->h_scalar) cudaFreeHost(c->h_scalar);
     if (c->part) ncclCommDestroy(c->part);
@@ -474,11 +485,13 @@ static gtcp_status halo_exchange(gtcp_ctx c, double* H) {
     int nt = c->prm.ntoroidal;
     int left = (c->rank_t - 1 + nt) % nt, right = (c->rank_t + 1) % nt;
     double* rb = c->halo_buf;  // [0]: from left (their P-1), [1..2]: from right (their 0, 1)
+    // sends: left then right; receives: right then left -- with two domains
+    // left == right and NCCL pairs same-peer messages in posting order.
     NC(ncclGroupStart());
     NC(ncclSend(p0, 2 * mg, ncclDouble, left, c->tor, c->st));
     NC(ncclSend(H + (long long)P * mg, mg, ncclDouble, right, c->tor, c->st));
-    NC(ncclRecv(rb, mg, ncclDouble, left, c->tor, c->st));
     NC(ncclRecv(rb + mg, 2 * mg, ncclDouble, right, c->tor, c->st));
+    NC(ncclRecv(rb, mg, ncclDouble, left, c->tor, c->st));
     NC(ncclGroupEnd());
     if (c->rank_t == 0) launch_seam_rotate(g, rb, pm1, -1, c->st);
     else CU(cudaMemcpyAsync(pm1, rb, mg * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
@@ -1005,6 +1018,81 @@ extern "C" gtcp_status gtcp_set_charge_mode(gtcp_ctx c, int mode) {
 // shift over NCCL (toroidal ring neighbours), H-1..H-3
 // ----------------------------------------------------------------------------
 gtcp_status shift_exchange(gtcp_ctx c) {
-    (void)c;
-    return set_err(c, GTCP_EINVAL, "shift: multi-domain shift not built yet");
+    const Geo& g = c->geo;
+    const int nt = c->prm.ntoroidal;
+    const int left = (c->rank_t - 1 + nt) % nt, right = (c->rank_t + 1) % nt;
+    // movers carry the live state and mu, plus the saved RK2 state mid-step (H-3)
+    const int nattr = (c->stage_next == 2) ? 11 : 6;
+    long long start = 0;  // first pass scans everything, later passes only the arrivals
+    for (int iter = 0; iter <= nt; iter++) {
+        double* attrs[11];
+        for (int d = 0; d < 5; d++) attrs[d] = c->live[d] + start;
+        attrs[5] = c->mu + start;
+        for (int d = 0; d < 5; d++) attrs[6 + d] = c->saved[d] + start;
+        unsigned long long* idp = c->id ? c->id + start : nullptr;
+        const long long n = c->n - start;
+        const int nb = (int)std::max<long long>(1, (n + 1023) / 1024);
+        unsigned* cntL = c->bcount;
+        unsigned* cntR = cntL + (c->shift_blocks + 1);
+        unsigned* cntH = cntR + (c->shift_blocks + 1);
+        unsigned* cntF = cntH + (c->shift_blocks + 1);
+        unsigned* offL = cntF + (c->shift_blocks + 1);
+        unsigned* offR = offL + (c->shift_blocks + 1);
+        unsigned* offH = offR + (c->shift_blocks + 1);
+        unsigned* offF = offH + (c->shift_blocks + 1);
+        launch_shift_classify(g, attrs[2], n, c->cls, cntL, cntR, c->st);
+        launch_scan_u32(cntL, offL, nb, c->scan_tmp, c->st);
+        launch_scan_u32(cntR, offR, nb, c->scan_tmp, c->st);
+        launch_shift_nkeep(n, offL + nb, offR + nb, c->d_nkeep, c->d_counts, c->st);
+        // counts: mine (left, right) out; theirs in; global mover total
+        NC(ncclGroupStart());
+        NC(ncclSend(c->d_counts + 0, 1, ncclInt64, left, c->tor, c->st));
+        NC(ncclSend(c->d_counts + 1, 1, ncclInt64, right, c->tor, c->st));
+        NC(ncclRecv(c->d_counts + 2, 1, ncclInt64, right, c->tor, c->st));  // right's left-movers
+        NC(ncclRecv(c->d_counts + 3, 1, ncclInt64, left, c->tor, c->st));   // left's right-movers
+        NC(ncclGroupEnd());
+        launch_sum_i64_pair(c->d_counts, c->d_counts + 4, c->st);
+        NC(ncclAllReduce(c->d_counts + 4, c->d_counts + 5, 1, ncclInt64, ncclSum, c->tor, c->st));
+        CU(cudaMemcpyAsync(c->h_counts, c->d_counts, 6 * sizeof(long long), cudaMemcpyDeviceToHost, c->st));
+        CU(cudaStreamSynchronize(c->st));
+        const long long nL = c->h_counts[0], nR = c->h_counts[1], rR = c->h_counts[2], rL = c->h_counts[3];
+        const long long total = c->h_counts[5];
+        if (total == 0) break;
+        if (nL > c->shift_cap || nR > c->shift_cap)
+            return set_err(c, GTCP_ECAPACITY, "shift: send buffer overflow");
+        const long long nkeep = n - nL - nR;
+        if (start + nkeep + rL + rR > c->cap) return set_err(c, GTCP_ECAPACITY, "shift: particle capacity exceeded");
+        if (nL + nR > 0) {
+            launch_shift_pack(attrs, nattr, idp, c->cls, n, offL, offR, c->sendL, c->sendR, c->sidL, c->sidR, c->st);
+            launch_shift_count_holes(c->cls, n, c->d_nkeep, cntH, cntF, c->st);
+            launch_scan_u32(cntH, offH, nb, c->scan_tmp, c->st);
+            launch_scan_u32(cntF, offF, nb, c->scan_tmp, c->st);
+            launch_shift_backfill(attrs, nattr, idp, c->cls, n, c->d_nkeep, offH, offF, c->holes, c->st);
+        }
+        KCHECK();
+        // payload: straight into the particle arrays behind the keepers
+        NC(ncclGroupStart());
+        for (int d = 0; d < nattr; d++) {
+            NC(ncclSend(c->sendL[d], nL, ncclDouble, left, c->tor, c->st));
+            NC(ncclSend(c->sendR[d], nR, ncclDouble, right, c->tor, c->st));
+            NC(ncclRecv(attrs[d] + nkeep, rR, ncclDouble, right, c->tor, c->st));
+            NC(ncclRecv(attrs[d] + nkeep + rR, rL, ncclDouble, left, c->tor, c->st));
+        }
+        if (idp) {
+            NC(ncclSend(c->sidL, nL, ncclUint64, left, c->tor, c->st));
+            NC(ncclSend(c->sidR, nR, ncclUint64, right, c->tor, c->st));
+            NC(ncclRecv(idp + nkeep, rR, ncclUint64, right, c->tor, c->st));
+            NC(ncclRecv(idp + nkeep + rR, rL, ncclUint64, left, c->tor, c->st));
+        }
+        NC(ncclGroupEnd());
+        c->movers_sent += nL + nR;
+        c->movers_recv += rL + rR;
+        c->n = start + nkeep + rL + rR;
+        start = start + nkeep;  // only the arrivals can still be misplaced
+    }
+    // max |w| of the live state changed with the particle set
+    CU(cudaMemsetAsync(&c->dc->wmax_bits, 0, 8, c->st));
+    launch_wmax(c->live[4], c->n, c->dc, c->st);
+    KCHECK();
+    return GTCP_OK;
 }

@@ -969,6 +969,13 @@ void launch_sum_f64(const double* x, long long n, double* out, double* partial, 
     g_launches += 2;
 }
 
+__global__ void k_sum_i64_pair(const long long* in2, long long* out) { out[0] = in2[0] + in2[1]; }
+
+void launch_sum_i64_pair(const long long* in2, long long* out, cudaStream_t st) {
+    k_sum_i64_pair<<<1, 1, 0, st>>>(in2, out);
+    g_launches++;
+}
+
 __global__ void k_fill_f64(double* __restrict__ x, long long n, double v) {
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x)
         x[p] = v;

@@ -292,3 +292,26 @@ def test_device_loader_statistics(G):
     assert abs((parts["mu"] * B).mean() - 1.0) < 1e-2
     assert r.min() >= cfg["a0"] and r.max() <= cfg["a1"]
     assert parts["zeta"].min() >= 0 and parts["zeta"].max() < 4 * TWO_PI / 4 + 1e-12
+
+
+# ------------------------------------------------------------------ multi-GPU
+def _ngpus():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("args", [["--size", "T", "--mzetamax", "8"], ["--size", "A", "--n", "1000000"]])
+def test_toroidal_decomposition_parity_2gpu(G, args):
+    """Toroidal decomposition over 2 GPUs (NCCL shift, ghost-plane charge
+    merge, halo exchange) against the oracle's single-domain step."""
+    import os
+    import subprocess
+    import sys
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "tools", "dist_parity.py")] + args
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert '"ok": true' in r.stdout
