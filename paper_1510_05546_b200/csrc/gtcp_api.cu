@@ -75,6 +75,8 @@ struct gtcp_ctx_s {
     unsigned char* cls = nullptr;
     unsigned* bcount = nullptr;  // per-block counts and offsets (8 arrays of shift_blocks+1)
     unsigned* holes = nullptr;   // hole positions, shift_cap
+    unsigned* fills = nullptr;   // filler positions, shift_cap
+    unsigned* midx = nullptr;    // mover positions (left list, right list), 2 shift_cap
     long long* d_nkeep = nullptr;
     long long* d_counts = nullptr;  // [myL, myR, fromRight, fromLeft, mine, total]
     long long* h_counts = nullptr;  // pinned mirror
@@ -402,7 +404,9 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
         CU(dalloc(&c->cls, c->cap));
         c->shift_blocks = (int)((c->cap + 1023) / 1024);
         CU(dalloc(&c->bcount, 8LL * (c->shift_blocks + 1)));
-        CU(dalloc(&c->holes, c->shift_cap));
+        CU(dalloc(&c->holes, 2 * c->shift_cap));
+        CU(dalloc(&c->fills, 2 * c->shift_cap));
+        CU(dalloc(&c->midx, 2 * c->shift_cap));
         CU(dalloc(&c->d_nkeep, 1));
         CU(dalloc(&c->d_counts, 8));
         CU(cudaMallocHost((void**)&c->h_counts, 8 * sizeof(long long)));
@@ -429,7 +433,7 @@ extern "C" void gtcp_destroy(gtcp_ctx c) {
     F(c->gfield); F(c->nm); F(c->ringsum); F(c->phi00); F(c->halo_buf); F(c->fx_recv); F(c->dc); F(c->d_scalar); F(c->d_partial);
     F(c->d_mtheta); F(c->d_igrid); F(c->d_itran); F(c->d_qtinv);
     for (int d = 0; d < 12; d++) { F(c->sendL[d]); F(c->sendR[d]); F(c->recvL[d]); F(c->recvR[d]); }
-    F(c->sidL); F(c->sidR); F(c->ridL); F(c->ridR); F(c->cls); F(c->bcount); F(c->holes); F(c->d_nkeep);
+    F(c->sidL); F(c->sidR); F(c->ridL); F(c->ridR); F(c->cls); F(c->bcount); F(c->holes); F(c->fills); F(c->midx); F(c->d_nkeep);
     F(c->d_counts);
     if (c->h_counts) cudaFreeHost(c->h_counts);
     if (c->h_dc) cudaFreeHost(c->h_dc);
@@ -1018,6 +1022,17 @@ extern "C" gtcp_status gtcp_set_charge_mode(gtcp_ctx c, int mode) {
 // shift over NCCL (toroidal ring neighbours), H-1..H-3
 // ----------------------------------------------------------------------------
 gtcp_status shift_exchange(gtcp_ctx c) {
+    static const bool prof = getenv("GTCP_PROFILE_SHIFT") != nullptr;
+    cudaEvent_t ev[16];
+    int nev = 0;
+    auto mark = [&]() {
+        if (prof && nev < 16) {
+            cudaEventCreate(&ev[nev]);
+            cudaEventRecord(ev[nev], c->st);
+            nev++;
+        }
+    };
+    mark();
     const Geo& g = c->geo;
     const int nt = c->prm.ntoroidal;
     const int left = (c->rank_t - 1 + nt) % nt, right = (c->rank_t + 1) % nt;
@@ -1031,7 +1046,7 @@ gtcp_status shift_exchange(gtcp_ctx c) {
         for (int d = 0; d < 5; d++) attrs[6 + d] = c->saved[d] + start;
         unsigned long long* idp = c->id ? c->id + start : nullptr;
         const long long n = c->n - start;
-        const int nb = (int)std::max<long long>(1, (n + 1023) / 1024);
+        const int nb = shift_chunks(n);
         unsigned* cntL = c->bcount;
         unsigned* cntR = cntL + (c->shift_blocks + 1);
         unsigned* cntH = cntR + (c->shift_blocks + 1);
@@ -1044,6 +1059,7 @@ gtcp_status shift_exchange(gtcp_ctx c) {
         launch_scan_u32(cntL, offL, nb, c->scan_tmp, c->st);
         launch_scan_u32(cntR, offR, nb, c->scan_tmp, c->st);
         launch_shift_nkeep(n, offL + nb, offR + nb, c->d_nkeep, c->d_counts, c->st);
+        if (iter == 0) mark();
         // counts: mine (left, right) out; theirs in; global mover total
         NC(ncclGroupStart());
         NC(ncclSend(c->d_counts + 0, 1, ncclInt64, left, c->tor, c->st));
@@ -1054,6 +1070,7 @@ gtcp_status shift_exchange(gtcp_ctx c) {
         launch_sum_i64_pair(c->d_counts, c->d_counts + 4, c->st);
         NC(ncclAllReduce(c->d_counts + 4, c->d_counts + 5, 1, ncclInt64, ncclSum, c->tor, c->st));
         CU(cudaMemcpyAsync(c->h_counts, c->d_counts, 6 * sizeof(long long), cudaMemcpyDeviceToHost, c->st));
+        if (iter == 0) mark();
         CU(cudaStreamSynchronize(c->st));
         const long long nL = c->h_counts[0], nR = c->h_counts[1], rR = c->h_counts[2], rL = c->h_counts[3];
         const long long total = c->h_counts[5];
@@ -1062,14 +1079,21 @@ gtcp_status shift_exchange(gtcp_ctx c) {
             return set_err(c, GTCP_ECAPACITY, "shift: send buffer overflow");
         const long long nkeep = n - nL - nR;
         if (start + nkeep + rL + rR > c->cap) return set_err(c, GTCP_ECAPACITY, "shift: particle capacity exceeded");
+        if (iter == 0) mark();
         if (nL + nR > 0) {
-            launch_shift_pack(attrs, nattr, idp, c->cls, n, offL, offR, c->sendL, c->sendR, c->sidL, c->sidR, c->st);
+            launch_shift_pack(attrs, nattr, idp, c->cls, n, offL, offR, c->sendL, c->sendR, c->sidL, c->sidR, c->midx, nL, nR,
+                              c->st);
+            if (iter == 0) mark();
             launch_shift_count_holes(c->cls, n, c->d_nkeep, cntH, cntF, c->st);
             launch_scan_u32(cntH, offH, nb, c->scan_tmp, c->st);
             launch_scan_u32(cntF, offF, nb, c->scan_tmp, c->st);
-            launch_shift_backfill(attrs, nattr, idp, c->cls, n, c->d_nkeep, offH, offF, c->holes, c->st);
+            if (iter == 0) mark();
+            // holes below n_keep == movers below n_keep == fillers above it; their count is
+            // min(nL + nR, ...) -- bounded by the movers, so size the copy by nL + nR (extra threads idle)
+            launch_shift_backfill(attrs, nattr, idp, c->cls, n, c->d_nkeep, offH, offF, c->holes, c->fills, nL + nR, c->st);
         }
         KCHECK();
+        if (iter == 0) mark();
         // payload: straight into the particle arrays behind the keepers
         NC(ncclGroupStart());
         for (int d = 0; d < nattr; d++) {
@@ -1085,14 +1109,29 @@ gtcp_status shift_exchange(gtcp_ctx c) {
             NC(ncclRecv(idp + nkeep + rR, rL, ncclUint64, left, c->tor, c->st));
         }
         NC(ncclGroupEnd());
+        if (iter == 0) mark();
         c->movers_sent += nL + nR;
         c->movers_recv += rL + rR;
         c->n = start + nkeep + rL + rR;
         start = start + nkeep;  // only the arrivals can still be misplaced
     }
-    // max |w| of the live state changed with the particle set
-    CU(cudaMemsetAsync(&c->dc->wmax_bits, 0, 8, c->st));
-    launch_wmax(c->live[4], c->n, c->dc, c->st);
+    mark();
+    // the fixed-point charge scale needs a bound on max|w| of the new particle
+    // set: the max over the toroidal ranks is one (positive doubles order like
+    // their uint64 bit patterns), no pass over the weights needed
+    NC(ncclAllReduce(&c->dc->wmax_bits, &c->dc->wmax_bits, 1, ncclUint64, ncclMax, c->tor, c->st));
+    mark();
     KCHECK();
+    if (prof) {
+        cudaStreamSynchronize(c->st);
+        fprintf(stderr, "[shift r%d n=%lld]", c->rank, c->n);
+        for (int i = 1; i < nev; i++) {
+            float ms;
+            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            fprintf(stderr, " %.3f", ms);
+        }
+        fprintf(stderr, "\n");
+        for (int i = 0; i < nev; i++) cudaEventDestroy(ev[i]);
+    }
     return GTCP_OK;
 }

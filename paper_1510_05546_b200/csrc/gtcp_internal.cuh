@@ -110,6 +110,7 @@ void launch_ring_mean(const Geo& g, const double* ringsum, double* nm, cudaStrea
 void launch_sum_f64(const double* x, long long n, double* out, double* partial, cudaStream_t st);
 void launch_sum_i64_pair(const long long* in2, long long* out, cudaStream_t st);
 // shift (gtcp_shift.cu)
+int shift_chunks(long long n);
 void launch_shift_classify(const Geo& g, const double* zeta, long long n, unsigned char* cls, unsigned* cntL,
                            unsigned* cntR, cudaStream_t st);
 void launch_shift_nkeep(long long n, const unsigned* totL, const unsigned* totR, long long* nkeep, long long* counts,
@@ -118,10 +119,11 @@ void launch_shift_count_holes(const unsigned char* cls, long long n, const long 
                               unsigned* cntF, cudaStream_t st);
 void launch_shift_pack(double* const* attrs, int nattr, unsigned long long* id, const unsigned char* cls, long long n,
                        const unsigned* offL, const unsigned* offR, double* const* sendL, double* const* sendR,
-                       unsigned long long* idL, unsigned long long* idR, cudaStream_t st);
+                       unsigned long long* idL, unsigned long long* idR, unsigned* idx, long long nL, long long nR,
+                       cudaStream_t st);
 void launch_shift_backfill(double* const* attrs, int nattr, unsigned long long* id, const unsigned char* cls,
                            long long n, const long long* nkeep, const unsigned* offH, const unsigned* offF,
-                           unsigned* holes, cudaStream_t st);
+                           unsigned* holes, unsigned* fills, long long nholes, cudaStream_t st);
 void launch_fill_f64(double* x, long long n, double v, cudaStream_t st);
 void launch_gather_f64(const double* src, const long long* idx, long long m, double* out, cudaStream_t st);
 

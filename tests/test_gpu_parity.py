@@ -300,7 +300,7 @@ def _ngpus():
     return torch.cuda.device_count()
 
 
-@pytest.mark.parametrize("args", [["--size", "T", "--mzetamax", "8"], ["--size", "A", "--n", "1000000"]])
+@pytest.mark.parametrize("args", [["--size", "T", "--mzetamax", "8"], ["--size", "A", "--nparts", "1000000"]])
 def test_toroidal_decomposition_parity_2gpu(G, args):
     """Toroidal decomposition over 2 GPUs (NCCL shift, ghost-plane charge
     merge, halo exchange) against the oracle's single-domain step."""

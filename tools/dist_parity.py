@@ -23,7 +23,7 @@ import synth  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--size", default="T")
-ap.add_argument("--n", type=int, default=0, help="markers (0 = micell*(mgrid-mpsi)*mzetamax)")
+ap.add_argument("--nparts", type=int, default=0, help="markers (0 = micell*(mgrid-mpsi)*mzetamax)")
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--w-amp", type=float, default=None)
 ap.add_argument("--mzetamax", type=int, default=None)
@@ -38,7 +38,7 @@ over = {"mzetamax": a.mzetamax} if a.mzetamax else {}
 cfg = synth.config(a.size, **over)
 params = G.gtcp_default_params(a.size, ntoroidal=world, track_ids=1, bin_every=1, **over)
 geo = G.gtcp_geometry(params)
-n = a.n or cfg["micell"] * (geo["mgrid"] - cfg["mpsi"]) * cfg["mzetamax"]
+n = a.nparts or cfg["micell"] * (geo["mgrid"] - cfg["mpsi"]) * cfg["mzetamax"]
 parts = synth.load_particles(cfg, n, seed=1, w_amp=a.w_amp)
 P = cfg["mzetamax"] // world
 cz = cfg["mzetamax"] / (2.0 * math.pi)
