@@ -310,6 +310,7 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     long long n_load = per_plane * P / p->npartdom;
     double headroom = nranks > 1 ? 0.10 : 0.0;
     c->cap = (long long)std::ceil(n_load * (p->capacity_factor + headroom)) + 1024;
+    c->cap = (c->cap + 255) / 256 * 256;  // TMA-staged kernels copy whole 16-byte granules of 256-particle chunks
     for (int d = 0; d < 5; d++) {
         CU(dalloc(&c->bufA[d], c->cap));
         CU(dalloc(&c->bufB[d], c->cap));

@@ -279,6 +279,7 @@ __device__ __forceinline__ int win_nodes(const Geo& g, int i, int c0, int c1, do
     int m_lo = max(0, i - h), m_hi = min(g.mpsi, i + 1 + h);
     int S = 0;
     for (int m = m_lo; m <= m_hi; m++) S += win_width(g, i, c0, c1, m, rho_cut);
+    S += (16 - (S & 31) + 32) & 31;  // the plane-stride padding of k_deposit_tiled
     return S * (g.P + 1);
 }
 
@@ -348,6 +349,9 @@ __global__ void __launch_bounds__(kDepositThreads, 3)
                 T.mt[q] = __ldg(g.mtheta + m);
                 S += W;
             }
+            // pad the plane stride to 16 (mod 32) words: the lane bit that picks
+            // plane k or k+1 then always flips the shared-memory bank half
+            S += (16 - (S & 31) + 32) & 31;
             T.S = S;
             T.total = S * P1;
             if (T.total > cap_nodes) {  // window too large for shared memory: everything via L2
@@ -376,6 +380,7 @@ __global__ void __launch_bounds__(kDepositThreads, 3)
             }
             for (int q = 0; q < T.nr; q++)
                 for (int x = threadIdx.x; x < T.WO[q].x; x += blockDim.x) colq[T.WO[q].y + x] = (unsigned char)q;
+            // padding columns (never hit) map to the last ring; they stay zero and are skipped by the flush
             uint4* z4 = reinterpret_cast<uint4*>(slo);
             const int nz = (2 * (cap_nodes + 1)) / 4;  // both limb arrays are contiguous
             const int nzt = (2 * T.total + 3) / 4;
@@ -408,12 +413,15 @@ __global__ void __launch_bounds__(kDepositThreads, 3)
             const double wzl = __dmul_rn(__dsub_rn(1.0, wz1), ws), wzu = __dmul_rn(wz1, ws);
             const double rho_r = __dmul_rn(rho, inv_r);
 #pragma unroll
-            for (int l = 0; l < 4; l++) {
-                double rl = r, tl2 = theta;
-                if (l == 0) rl = __dadd_rn(r, rho);
-                if (l == 2) rl = __dsub_rn(r, rho);
-                if (l == 1) tl2 = __dadd_rn(theta, rho_r);
-                if (l == 3) tl2 = __dsub_rn(theta, rho_r);
+            for (int lq = 0; lq < 4; lq++) {
+                // lane-rotated gyro-point: l = (lq + lane) mod 4.  r +- rho and
+                // theta +- rho/r as fma(sign, x, y): one rounding, bit-identical
+                // to the add/sub of the direct kernel (sign in {-1, 0, 1})
+                const int l = (lq + lane) & 3;
+                const double sr = (double)(((l + 1) & 1) * (1 - (l & 2)));
+                const double stt = (double)((l & 1) * (1 - (l & 2)));
+                double rl = __fma_rn(sr, rho, r);
+                const double tl2 = __fma_rn(stt, rho_r, theta);
                 rl = fmin(fmax(rl, g.a0), g.a1);
                 const double x = __dmul_rn(__dsub_rn(rl, g.a0), g.inv_dr);
                 const int ir = min(max((int)floor(x), 0), g.mpsi - 1);
@@ -555,6 +563,114 @@ __device__ __forceinline__ double warp_max(double v) {
     return v;
 }
 
+// One RK2 stage of one particle (U-1..U-8): returns the new state X[5] from
+// the source state (psi, theta, zeta, rho_par, w), mu and the base state.
+// Counts reflections / plane clamps into the caller's registers.
+__device__ __forceinline__ void push_one(const Geo& g, double psi, double theta, double zeta, double rho_par,
+                                         double w, double mu, const double* base, double h,
+                                         const double* __restrict__ gf, double* X, long long& refl,
+                                         long long& clamps) {
+    // U-1
+    double st, ct;
+    sincos(theta, &st, &ct);
+    double r, invB, rho, inv_r;
+    gyro_radius(g, psi, ct, mu, &r, &invB, &rho, &inv_r);
+    const double eps = r * g.inv_R0;
+    const double q = g.q0 + g.q2 * r * r;
+    const double inv_qB = 1.0 / (q * invB);  // one division: 1/q and B follow
+    const double B = q * inv_qB;
+    const double inv_q = invB * inv_qB;
+    // U-2 gather
+    double wz1;
+    int kg = plane_of(g, zeta, &wz1);
+    int k = kg - g.k0;
+    if (k < 0 || k > g.P - 1) { clamps++; k = min(max(k, 0), g.P - 1); }
+    const double wz0 = 1.0 - wz1;
+    // accumulate each bounding plane separately (4 FMA per component and
+    // (point, ring)); the plane weights and the 1/4 per gyro-point are applied
+    // once at the end.  a0/a1 carry 1/4 already (gyro_stencil), so use 4*a.
+    double r0 = 0.0, t0 = 0.0, p0 = 0.0, r1 = 0.0, t1 = 0.0, p1 = 0.0;
+    const double* gk = gf + (long long)k * g.mgrid * 6;
+    gyro_stencil(g, r, theta, zeta, rho, inv_r, [&](int m, int j, int mt, double a0, double a1) {
+        const double2* qq = reinterpret_cast<const double2*>(gk + ((long long)__ldg(g.igrid + m) + j) * 6);
+        double2 v0 = __ldg(qq + 0), v1 = __ldg(qq + 1), v2 = __ldg(qq + 2);
+        double2 v3 = __ldg(qq + 3), v4 = __ldg(qq + 4), v5 = __ldg(qq + 5);
+        // node j: (v0.x v0.y v1.x) plane k, (v1.y v2.x v2.y) plane k+1; node j+1 likewise in v3..v5
+        r0 = fma(a0, v0.x, fma(a1, v3.x, r0));
+        t0 = fma(a0, v0.y, fma(a1, v3.y, t0));
+        p0 = fma(a0, v1.x, fma(a1, v4.x, p0));
+        r1 = fma(a0, v1.y, fma(a1, v4.y, r1));
+        t1 = fma(a0, v2.x, fma(a1, v5.x, t1));
+        p1 = fma(a0, v2.y, fma(a1, v5.y, p1));
+        (void)mt;
+    });
+    const double gr = wz0 * r0 + wz1 * r1, gt = wz0 * t0 + wz1 * t1, gp = wz0 * p0 + wz1 * p1;
+    // U-3 drifts
+    const double vpar = g.omega0 * B * rho_par;
+    const double iOB = g.inv_omega0 * invB;  // 1 / (omega0 B)
+    double vEr = 0.0, vEt = 0.0, vdr = 0.0, vdt = 0.0;
+    if (g.drifts) {
+        vEr = -gt * inv_r * iOB;
+        vEt = gr * iOB;
+        const double Cd = (vpar * vpar + mu * B) * g.inv_omega0_R0;
+        vdr = -Cd * st;
+        vdt = -Cd * ct;
+    }
+    // U-4
+    const double rdot = vEr + vdr;
+    const double psidot = r * rdot;
+    const double thdot = vpar * B * inv_q * g.inv_R0 + (vEt + vdt) * inv_r;
+    const double zdot = vpar * B * g.inv_R0;
+    // U-5
+    double vdot = -mu * B * B * B * r * st * inv_q * g.inv_R0 * g.inv_R0;
+    if (g.paranl) {
+        double par = -(B * g.inv_R0) * gp;
+        if (g.drifts) par += vpar * g.inv_omega0_R0 * (st * gr + ct * gt * inv_r);
+        vdot += par;
+    }
+    const double dBdr = -B * B * ct * g.inv_R0;
+    const double dBdt = B * B * eps * st;
+    const double Bdot = rdot * dBdr + thdot * dBdt;
+    const double rhodot = (vdot - vpar * Bdot * invB) * iOB;
+    // U-6 delta-f weight
+    const double Ekin = 0.5 * vpar * vpar + mu * B;
+    const double x6 = (r - 0.5) * (1.0 / 0.35);
+    const double x2 = x6 * x6;
+    const double prof = exp(-(x2 * x2 * x2));
+    const double kappa = prof * (g.rln + (Ekin - 1.5) * g.rlt) * g.inv_R0;
+    const double wdot = (1.0 - (double)g.paranl * w) *
+                        (vEr * kappa - (vpar * (B * g.inv_R0) * gp + vdr * gr + vdt * gt * inv_r));
+    // U-7 update
+    const double F[5] = {psidot, thdot, zdot, rhodot, wdot};
+#pragma unroll
+    for (int d = 0; d < 5; d++) X[d] = base[d] + h * F[d];
+    // U-8 wrap angles (same operation sequence as the oracle) and reflect r
+#pragma unroll
+    for (int d = 1; d <= 2; d++) {
+        // X in [0, 2 pi): floor(X / 2 pi) = 0 and the oracle's expression returns X itself
+        if (X[d] < 0.0 || X[d] >= GTCP_TWO_PI) {
+            double t = __dsub_rn(X[d], __dmul_rn(GTCP_TWO_PI, floor(__ddiv_rn(X[d], GTCP_TWO_PI))));
+            if (t >= GTCP_TWO_PI) t = 0.0;
+            X[d] = t;
+        }
+    }
+    double rn = sqrt(2.0 * fmax(X[0], 0.0));
+    bool rf = false;
+    if (rn > g.a1) { rn = 2.0 * g.a1 - rn; rf = true; }
+    if (rn < g.a0) { rn = 2.0 * g.a0 - rn; rf = true; }
+    if (rf) { X[0] = 0.5 * rn * rn; refl++; }
+}
+
+__device__ __forceinline__ void push_epilogue(DevCounters* dc, double wmax, long long refl, long long clamps,
+                                              int nonfinite) {
+    wmax = warp_max(wmax);
+    if ((threadIdx.x & 31) == 0 && wmax > 0.0)
+        atomicMax(&dc->wmax_bits, (unsigned long long)__double_as_longlong(wmax));
+    if (refl) atomicAdd((unsigned long long*)&dc->reflections, (unsigned long long)refl);
+    if (clamps) atomicAdd((unsigned long long*)&dc->plane_clamps, (unsigned long long)clamps);
+    if (nonfinite) dc->nonfinite = 1;
+}
+
 template <int MINB>
 __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long long n, double h,
                                              const double* __restrict__ gf, DevCounters* dc) {
@@ -563,103 +679,106 @@ __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long lon
     int nonfinite = 0;
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
          p += (long long)gridDim.x * blockDim.x) {
-        const double psi = pp.src[0][p], theta = pp.src[1][p], zeta = pp.src[2][p], rho_par = pp.src[3][p],
-                     w = pp.src[4][p], mu = pp.mu[p];
-        // U-1
-        double st, ct;
-        sincos(theta, &st, &ct);
-        double r, invB, rho, inv_r;
-        gyro_radius(g, psi, ct, mu, &r, &invB, &rho, &inv_r);
-        const double eps = r * g.inv_R0;
-        const double q = g.q0 + g.q2 * r * r;
-        const double inv_qB = 1.0 / (q * invB);  // one division: 1/q and B follow
-        const double B = q * inv_qB;
-        const double inv_q = invB * inv_qB;
-        // U-2 gather
-        double wz1;
-        int kg = plane_of(g, zeta, &wz1);
-        int k = kg - g.k0;
-        if (k < 0 || k > g.P - 1) { clamps++; k = min(max(k, 0), g.P - 1); }
-        const double wz0 = 1.0 - wz1;
-        double gr = 0.0, gt = 0.0, gp = 0.0;
-        const double* gk = gf + (long long)k * g.mgrid * 6;
-        gyro_stencil(g, r, theta, zeta, rho, inv_r, [&](int m, int j, int mt, double a0, double a1) {
-            const double2* qq = reinterpret_cast<const double2*>(gk + ((long long)__ldg(g.igrid + m) + j) * 6);
-            double2 v0 = __ldg(qq + 0), v1 = __ldg(qq + 1), v2 = __ldg(qq + 2);
-            double2 v3 = __ldg(qq + 3), v4 = __ldg(qq + 4), v5 = __ldg(qq + 5);
-            // node j: (v0.x v0.y v1.x) plane k, (v1.y v2.x v2.y) plane k+1; node j+1 likewise in v3..v5
-            double c00 = a0 * wz0, c01 = a0 * wz1, c10 = a1 * wz0, c11 = a1 * wz1;
-            gr += c00 * v0.x + c01 * v1.y + c10 * v3.x + c11 * v4.y;
-            gt += c00 * v0.y + c01 * v2.x + c10 * v3.y + c11 * v5.x;
-            gp += c00 * v1.x + c01 * v2.y + c10 * v4.x + c11 * v5.y;
-            (void)mt;
-        });
-        // U-3 drifts
-        const double vpar = g.omega0 * B * rho_par;
-        const double iOB = g.inv_omega0 * invB;  // 1 / (omega0 B)
-        double vEr = 0.0, vEt = 0.0, vdr = 0.0, vdt = 0.0;
-        if (g.drifts) {
-            vEr = -gt * inv_r * iOB;
-            vEt = gr * iOB;
-            const double Cd = (vpar * vpar + mu * B) * g.inv_omega0_R0;
-            vdr = -Cd * st;
-            vdt = -Cd * ct;
-        }
-        // U-4
-        const double rdot = vEr + vdr;
-        const double psidot = r * rdot;
-        const double thdot = vpar * B * inv_q * g.inv_R0 + (vEt + vdt) * inv_r;
-        const double zdot = vpar * B * g.inv_R0;
-        // U-5
-        double vdot = -mu * B * B * B * r * st * inv_q * g.inv_R0 * g.inv_R0;
-        if (g.paranl) {
-            double par = -(B * g.inv_R0) * gp;
-            if (g.drifts) par += vpar * g.inv_omega0_R0 * (st * gr + ct * gt * inv_r);
-            vdot += par;
-        }
-        const double dBdr = -B * B * ct * g.inv_R0;
-        const double dBdt = B * B * eps * st;
-        const double Bdot = rdot * dBdr + thdot * dBdt;
-        const double rhodot = (vdot - vpar * Bdot * invB) * iOB;
-        // U-6 delta-f weight
-        const double Ekin = 0.5 * vpar * vpar + mu * B;
-        const double x6 = (r - 0.5) * (1.0 / 0.35);
-        const double x2 = x6 * x6;
-        const double prof = exp(-(x2 * x2 * x2));
-        const double kappa = prof * (g.rln + (Ekin - 1.5) * g.rlt) * g.inv_R0;
-        const double wdot = (1.0 - (double)g.paranl * w) *
-                            (vEr * kappa - (vpar * (B * g.inv_R0) * gp + vdr * gr + vdt * gt * inv_r));
-        // U-7 update
-        double X[5];
-        const double F[5] = {psidot, thdot, zdot, rhodot, wdot};
+        double base[5], X[5];
 #pragma unroll
-        for (int d = 0; d < 5; d++) X[d] = pp.base[d][p] + h * F[d];
-        // U-8 wrap angles (same operation sequence as the oracle) and reflect r
-#pragma unroll
-        for (int d = 1; d <= 2; d++) {
-            // X in [0, 2 pi): floor(X / 2 pi) = 0 and the oracle's expression returns X itself
-            if (X[d] < 0.0 || X[d] >= GTCP_TWO_PI) {
-                double t = __dsub_rn(X[d], __dmul_rn(GTCP_TWO_PI, floor(__ddiv_rn(X[d], GTCP_TWO_PI))));
-                if (t >= GTCP_TWO_PI) t = 0.0;
-                X[d] = t;
-            }
-        }
-        double rn = sqrt(2.0 * fmax(X[0], 0.0));
-        bool rf = false;
-        if (rn > g.a1) { rn = 2.0 * g.a1 - rn; rf = true; }
-        if (rn < g.a0) { rn = 2.0 * g.a0 - rn; rf = true; }
-        if (rf) { X[0] = 0.5 * rn * rn; refl++; }
+        for (int d = 0; d < 5; d++) base[d] = pp.base[d][p];
+        push_one(g, pp.src[0][p], pp.src[1][p], pp.src[2][p], pp.src[3][p], pp.src[4][p], pp.mu[p], base, h, gf,
+                 X, refl, clamps);
         if (!(isfinite(X[0]) && isfinite(X[1]) && isfinite(X[2]) && isfinite(X[3]) && isfinite(X[4]))) nonfinite = 1;
 #pragma unroll
         for (int d = 0; d < 5; d++) pp.out[d][p] = X[d];
         wmax = fmax(wmax, fabs(X[4]));
     }
-    wmax = warp_max(wmax);
-    if ((threadIdx.x & 31) == 0 && wmax > 0.0)
-        atomicMax(&dc->wmax_bits, (unsigned long long)__double_as_longlong(wmax));
-    if (refl) atomicAdd((unsigned long long*)&dc->reflections, (unsigned long long)refl);
-    if (clamps) atomicAdd((unsigned long long*)&dc->plane_clamps, (unsigned long long)clamps);
-    if (nonfinite) dc->nonfinite = 1;
+    push_epilogue(dc, wmax, refl, clamps, nonfinite);
+}
+
+// ---------------------------------------------------------------------------
+// TMA-staged push: persistent CTAs stream chunks of kPC particles; one thread
+// issues cp.async.bulk copies of the chunk's SoA segments (6 arrays for stage
+// 1, 11 for stage 2) into a kNB-deep ring of shared-memory stage buffers with
+// mbarrier completion, so the particle streams' HBM latency overlaps the
+// previous chunks' gather + RHS work.
+// ---------------------------------------------------------------------------
+static constexpr int kPC = 256;  // particles per chunk (= threads per CTA)
+static constexpr int kNB = 4;    // stage buffers
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    unsigned ok = 0;
+    while (!ok) {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    }
+}
+
+template <int NARR>
+__global__ void __launch_bounds__(kPC, 2) k_push_tma(Geo g, PushPtrs pp, long long n, double h,
+                                                     const double* __restrict__ gf, DevCounters* dc) {
+    // NARR = 6: src 5 + mu (stage 1, base == src); NARR = 11: + base 5 (stage 2)
+    extern __shared__ __align__(128) double sbuf[];  // [kNB][NARR][kPC]
+    __shared__ __align__(8) unsigned long long full[kNB];
+    const long long nchunks = (n + kPC - 1) / kPC;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kNB; s++) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](long long c, int s) {
+        const long long p0 = c * kPC;
+        const long long cnt = min((long long)kPC, n - p0);
+        const unsigned bytes = (unsigned)(((cnt * 8) + 15) & ~15LL);  // arrays are padded to 256 elements
+        mbar_expect_tx(&full[s], bytes * NARR);
+        double* dst = sbuf + (size_t)s * NARR * kPC;
+#pragma unroll
+        for (int a = 0; a < NARR; a++) {
+            const double* src = a < 5 ? pp.src[a] : (a == 5 ? pp.mu : pp.base[a - 6]);
+            bulk_g2s(dst + a * kPC, src + p0, bytes, &full[s]);
+        }
+    };
+    if (threadIdx.x == 0)
+        for (int s = 0; s < kNB; s++) {
+            long long c = blockIdx.x + (long long)s * gridDim.x;
+            if (c < nchunks) issue(c, s);
+        }
+    double wmax = 0.0;
+    long long refl = 0, clamps = 0;
+    int nonfinite = 0;
+    int it = 0;
+    for (long long c = blockIdx.x; c < nchunks; c += gridDim.x, it++) {
+        const int s = it % kNB;
+        mbar_wait(&full[s], (unsigned)((it / kNB) & 1));
+        const double* sb = sbuf + (size_t)s * NARR * kPC;
+        const long long p = c * kPC + threadIdx.x;
+        if (p < n) {
+            const int t = threadIdx.x;
+            double base[5], X[5];
+#pragma unroll
+            for (int d = 0; d < 5; d++) base[d] = (NARR == 11) ? sb[(6 + d) * kPC + t] : sb[d * kPC + t];
+            push_one(g, sb[0 * kPC + t], sb[1 * kPC + t], sb[2 * kPC + t], sb[3 * kPC + t], sb[4 * kPC + t],
+                     sb[5 * kPC + t], base, h, gf, X, refl, clamps);
+            if (!(isfinite(X[0]) && isfinite(X[1]) && isfinite(X[2]) && isfinite(X[3]) && isfinite(X[4])))
+                nonfinite = 1;
+#pragma unroll
+            for (int d = 0; d < 5; d++) pp.out[d][p] = X[d];
+            wmax = fmax(wmax, fabs(X[4]));
+        }
+        __syncthreads();  // everyone is done with buffer s: refill it
+        if (threadIdx.x == 0) {
+            long long cn = c + (long long)kNB * gridDim.x;
+            if (cn < nchunks) issue(cn, s);
+        }
+    }
+    push_epilogue(dc, wmax, refl, clamps, nonfinite);
 }
 
 void launch_push3(const Geo& g, const double* const src[5], const double* const base[5], double* const out[5],
@@ -673,14 +792,35 @@ void launch_push3(const Geo& g, const double* const src[5], const double* const 
         pp.out[d] = out[d];
     }
     pp.mu = mu;
-    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
-    static int minb = [] {
-        const char* e = getenv("GTCP_PUSH_MINB");
+    static int variant = [] {
+        const char* e = getenv("GTCP_PUSH_VARIANT");
         return e ? atoi(e) : 2;
     }();
-    if (minb == 3) k_push<3><<<blocks, 256, 0, st>>>(g, pp, n, h, gfield, dc);
-    else if (minb == 1) k_push<1><<<blocks, 256, 0, st>>>(g, pp, n, h, gfield, dc);
-    else k_push<2><<<blocks, 256, 0, st>>>(g, pp, n, h, gfield, dc);
+    const bool stage2 = (base[0] != src[0]);
+    if (variant == 0) {
+        // TMA-staged persistent kernel, 2 CTAs per SM
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+        long long nch = (n + kPC - 1) / kPC;
+        int blocks = (int)std::min<long long>(nch, 2LL * nsm);
+        if (stage2) {
+            size_t sm = (size_t)kNB * 11 * kPC * sizeof(double);
+            static bool cfg = (cudaFuncSetAttribute(k_push_tma<11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)sm) == cudaSuccess);
+            (void)cfg;
+            k_push_tma<11><<<blocks, kPC, sm, st>>>(g, pp, n, h, gfield, dc);
+        } else {
+            size_t sm = (size_t)kNB * 6 * kPC * sizeof(double);
+            static bool cfg = (cudaFuncSetAttribute(k_push_tma<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)sm) == cudaSuccess);
+            (void)cfg;
+            k_push_tma<6><<<blocks, kPC, sm, st>>>(g, pp, n, h, gfield, dc);
+        }
+    } else {
+        int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
+        if (variant == 3) k_push<3><<<blocks, 256, 0, st>>>(g, pp, n, h, gfield, dc);
+        else k_push<2><<<blocks, 256, 0, st>>>(g, pp, n, h, gfield, dc);
+    }
     g_launches++;
 }
 
