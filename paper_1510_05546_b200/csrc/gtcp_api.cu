@@ -29,6 +29,7 @@ struct gtcp_ctx_s {
     std::vector<double> qtinv;
     int mgrid = 0, P = 0, k0 = 0;
     int *d_mtheta = nullptr, *d_igrid = nullptr, *d_itran = nullptr;
+    unsigned short* d_node_ring = nullptr;
     double* d_qtinv = nullptr;
     Geo geo;
     // particles
@@ -293,6 +294,13 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     CU(cudaMemcpy(c->d_igrid, c->igrid.data(), sizeof(int) * (M + 2), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(c->d_itran, c->itran.data(), sizeof(int) * (M + 1), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(c->d_qtinv, c->qtinv.data(), sizeof(double) * (M + 1), cudaMemcpyHostToDevice));
+    {
+        std::vector<unsigned short> nr(mg);
+        for (int i = 0; i <= M; i++)
+            for (int j = c->igrid[i]; j < c->igrid[i + 1]; j++) nr[j] = (unsigned short)i;
+        CU(dalloc(&c->d_node_ring, mg));
+        CU(cudaMemcpy(c->d_node_ring, nr.data(), sizeof(unsigned short) * mg, cudaMemcpyHostToDevice));
+    }
     Geo& g = c->geo;
     g.mpsi = M; g.mzetamax = p->mzetamax; g.P = P; g.k0 = c->k0; g.ntor = p->ntoroidal; g.rank_t = c->rank_t;
     g.mgrid = mg; g.paranl = p->paranl; g.drifts = p->drifts;
@@ -305,6 +313,7 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     g.inv_omega0 = 1.0 / p->omega0;
     g.inv_omega0_R0 = 1.0 / (p->omega0 * p->R0);
     g.mtheta = c->d_mtheta; g.igrid = c->d_igrid; g.itran = c->d_itran; g.qtinv = c->d_qtinv;
+    g.node_ring = c->d_node_ring;
     // particle capacity: the loaded count plus headroom for shift imbalance
     long long per_plane = (long long)p->micell * (mg - M);
     long long n_load = per_plane * P / p->npartdom;
@@ -432,7 +441,7 @@ extern "C" void gtcp_destroy(gtcp_ctx c) {
     F(c->key); F(c->rankbuf); F(c->count); F(c->offset); F(c->scan_tmp); F(c->tiles);
     F(c->fx); F(c->rhoH); F(c->dnH); F(c->tmpH); F(c->phiH); F(c->rhs); F(c->jphi); F(c->g1); F(c->g2);
     F(c->gfield); F(c->nm); F(c->ringsum); F(c->phi00); F(c->halo_buf); F(c->fx_recv); F(c->dc); F(c->d_scalar); F(c->d_partial);
-    F(c->d_mtheta); F(c->d_igrid); F(c->d_itran); F(c->d_qtinv);
+    F(c->d_mtheta); F(c->d_igrid); F(c->d_itran); F(c->d_qtinv); F(c->d_node_ring);
     for (int d = 0; d < 12; d++) { F(c->sendL[d]); F(c->sendR[d]); F(c->recvL[d]); F(c->recvR[d]); }
     F(c->sidL); F(c->sidR); F(c->ridL); F(c->ridR); F(c->cls); F(c->bcount); F(c->holes); F(c->fills); F(c->midx); F(c->d_nkeep);
     F(c->d_counts);
@@ -625,8 +634,7 @@ extern "C" gtcp_status gtcp_poisson_smooth(gtcp_ctx c) {
     launch_jacobi_init(g, c->dnH, c->ringsum, c->rhs, c->jphi, c->st);
     for (int it = 0; it < c->prm.poisson_iters; it++) {
         launch_gyro(g, c->jphi, c->g1, c->st);
-        launch_gyro(g, c->g1, c->g2, c->st);
-        launch_jacobi_update(g, c->rhs, c->g2, c->jphi, c->prm.jacobi_omega, c->st);
+        launch_gyro_jacobi(g, c->g1, c->rhs, c->jphi, c->prm.jacobi_omega, c->st);
     }
     launch_zonal(g, c->ringsum, c->phi00, c->st);
     launch_add_zonal2(g, c->phi00, c->jphi, c->phiH, c->st);
@@ -686,6 +694,8 @@ static gtcp_status do_bin(gtcp_ctx c) {
     launch_bin_keys(g, s, c->n, c->key, c->rankbuf, c->count, c->st);
     launch_scan_u32(c->count, c->offset, c->nkeys, c->scan_tmp, c->st);
     launch_bin_dest(c->key, c->rankbuf, c->offset, c->n, c->rankbuf, c->st);
+    // gather form: inv[dest[p]] = p once, then every array is written coalesced
+    launch_perm_inverse(c->rankbuf, c->n, c->key, c->st);
     // permute live state, mu (and the saved state when mid-step) with one scratch array
     std::vector<double**> arrs;
     for (int d = 0; d < 5; d++) arrs.push_back(&c->live[d]);
@@ -693,7 +703,7 @@ static gtcp_status do_bin(gtcp_ctx c) {
     if (c->stage_next == 2)
         for (int d = 0; d < 5; d++) arrs.push_back(&c->saved[d]);
     for (double** a : arrs) {
-        launch_permute_f64(*a, c->scratch, c->rankbuf, c->n, c->st);
+        launch_gather_perm_f64(*a, c->scratch, c->key, c->n, c->st);
         // keep bufA/bufB bookkeeping consistent: the scratch becomes the array
         double* old = *a;
         for (int d = 0; d < 5; d++) {
@@ -704,7 +714,7 @@ static gtcp_status do_bin(gtcp_ctx c) {
         c->scratch = old;
     }
     if (c->id) {
-        launch_permute_u64(c->id, c->id_scratch, c->rankbuf, c->n, c->st);
+        launch_gather_perm_u64(c->id, c->id_scratch, c->key, c->n, c->st);
         std::swap(c->id, c->id_scratch);
     }
     launch_build_tiles(g, c->offset, c->tile_max, c->tiles, c->max_tiles, c->dc, c->dep_cap_nodes, c->st);

@@ -11,14 +11,7 @@ namespace gtcp {
 
 static constexpr double kInvTwoPi = 1.0 / GTCP_TWO_PI;
 
-__device__ __forceinline__ int ring_of(const Geo& g, int node) {
-    int lo = 0, hi = g.mpsi;  // largest i with igrid[i] <= node
-    while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (__ldg(g.igrid + mid) <= node) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
+__device__ __forceinline__ int ring_of(const Geo& g, int node) { return __ldg(g.node_ring + node); }
 
 static int blocks_for(long long n, int t = 256) {
     long long b = (n + t - 1) / t;
@@ -281,6 +274,35 @@ __global__ void k_jacobi_update(Geo g, const double* __restrict__ rhs, const dou
         double v = (1.0 - omega) * phi[e] + omega * (rhs[e] + g2[e]) / c0;
         phi[e] = (i == 0 || i == g.mpsi) ? 0.0 : v;
     }
+}
+
+// second G application fused with the Jacobi update (F-2):
+// phi <- (1-omega) phi + omega (rhs + G(g1)) / (1 + 1/tau), phi = 0 on rings 0, mpsi
+__global__ void k_gyro_jacobi(Geo g, const double* __restrict__ g1, const double* __restrict__ rhs,
+                              double* __restrict__ phi, double omega) {
+    long long total = (long long)g.P * g.mgrid;
+    const double c0 = 1.0 + 1.0 / g.tau;
+    GRID_LOOP(e, total) {
+        int k = (int)(e / g.mgrid), node = (int)(e % g.mgrid);
+        int i = ring_of(g, node);
+        if (i == 0 || i == g.mpsi) { phi[e] = 0.0; continue; }
+        int mt = __ldg(g.mtheta + i);
+        int j = node - __ldg(g.igrid + i);
+        if (j == mt) j = 0;
+        const double* pl = g1 + (long long)k * g.mgrid;
+        double zk = (double)(g.k0 + k) * g.dzeta;
+        double r = g.a0 + i * g.dr;
+        double th = j * (GTCP_TWO_PI / mt) + zk * __ldg(g.qtinv + i);
+        double v = plane_interp(g, pl, r + g.rhoG, th, zk) + plane_interp(g, pl, r, th + g.rhoG / r, zk) +
+                   plane_interp(g, pl, r - g.rhoG, th, zk) + plane_interp(g, pl, r, th - g.rhoG / r, zk);
+        phi[e] = (1.0 - omega) * phi[e] + omega * (rhs[e] + 0.25 * v) / c0;
+    }
+}
+
+void launch_gyro_jacobi(const Geo& g, const double* g1, const double* rhs, double* phi, double omega,
+                        cudaStream_t st) {
+    k_gyro_jacobi<<<blocks_for((long long)g.P * g.mgrid), 256, 0, st>>>(g, g1, rhs, phi, omega);
+    g_launches++;
 }
 
 void launch_jacobi_update(const Geo& g, const double* rhs, const double* g2, double* phi, double omega,

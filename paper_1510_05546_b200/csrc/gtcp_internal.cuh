@@ -27,6 +27,7 @@ struct Geo {
     const int* igrid;              // [mpsi+2]
     const int* itran;              // [mpsi+1]
     const double* qtinv;           // [mpsi+1]
+    const unsigned short* node_ring;  // [mgrid] ring of each node (replaces a binary search)
 };
 
 // One charge tile: particles [start, end) of the cell-sorted store whose
@@ -79,6 +80,10 @@ void launch_bin_keys(const Geo& g, const PSet& s, long long n, unsigned* key, un
 void launch_scan_u32(const unsigned* in, unsigned* out, long long n, unsigned* block_tmp, cudaStream_t st);
 void launch_bin_dest(const unsigned* key, const unsigned* rank, const unsigned* offset, long long n,
                      unsigned* dest, cudaStream_t st);
+void launch_perm_inverse(const unsigned* dest, long long n, unsigned* inv, cudaStream_t st);
+void launch_gather_perm_f64(const double* src, double* dst, const unsigned* inv, long long n, cudaStream_t st);
+void launch_gather_perm_u64(const unsigned long long* src, unsigned long long* dst, const unsigned* inv, long long n,
+                            cudaStream_t st);
 void launch_permute_f64(const double* src, double* dst, const unsigned* dest, long long n, cudaStream_t st);
 void launch_permute_u64(const unsigned long long* src, unsigned long long* dst, const unsigned* dest,
                         long long n, cudaStream_t st);
@@ -98,6 +103,8 @@ void launch_ring_sum(const Geo& g, const double* f, double* ringsum, cudaStream_
 void launch_jacobi_init(const Geo& g, const double* dn, const double* ringsum, double* rhs, double* phi,
                         cudaStream_t st);
 void launch_gyro(const Geo& g, const double* in, double* out, cudaStream_t st);
+void launch_gyro_jacobi(const Geo& g, const double* g1, const double* rhs, double* phi, double omega,
+                        cudaStream_t st);
 void launch_jacobi_update(const Geo& g, const double* rhs, const double* g2, double* phi, double omega,
                           cudaStream_t st);
 void launch_zonal(const Geo& g, const double* ringsum, double* phi00, cudaStream_t st);

@@ -977,6 +977,44 @@ void launch_bin_dest(const unsigned* key, const unsigned* rank, const unsigned* 
     g_launches++;
 }
 
+// inverse permutation: inv[dest[p]] = p
+__global__ void k_perm_inverse(const unsigned* __restrict__ dest, long long n, unsigned* __restrict__ inv) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x)
+        inv[dest[p]] = (unsigned)p;
+}
+
+void launch_perm_inverse(const unsigned* dest, long long n, unsigned* inv, cudaStream_t st) {
+    if (n <= 0) return;
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    k_perm_inverse<<<blocks, 256, 0, st>>>(dest, n, inv);
+    g_launches++;
+}
+
+// gather form of the permutation: dst[i] = src[inv[i]] (coalesced writes)
+template <class T>
+__global__ void k_gather_perm(const T* __restrict__ src, T* __restrict__ dst, const unsigned* __restrict__ inv,
+                              long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        dst[i] = __ldg(src + inv[i]);
+}
+
+void launch_gather_perm_f64(const double* src, double* dst, const unsigned* inv, long long n, cudaStream_t st) {
+    if (n <= 0) return;
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    k_gather_perm<double><<<blocks, 256, 0, st>>>(src, dst, inv, n);
+    g_launches++;
+}
+
+void launch_gather_perm_u64(const unsigned long long* src, unsigned long long* dst, const unsigned* inv, long long n,
+                            cudaStream_t st) {
+    if (n <= 0) return;
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    k_gather_perm<unsigned long long><<<blocks, 256, 0, st>>>(src, dst, inv, n);
+    g_launches++;
+}
+
 __global__ void k_permute_f64(const double* __restrict__ src, double* __restrict__ dst,
                               const unsigned* __restrict__ dest, long long n) {
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
@@ -1013,6 +1051,18 @@ __device__ __forceinline__ int ring_tiles(const Geo& g, int i, const unsigned* o
                                           Tile* out, int max_out, int cap_nodes, double rho_cut) {
     int mt = __ldg(g.mtheta + i), ig = __ldg(g.igrid + i);
     int nt = 0;
+    // largest label span whose window fits the shared-memory capacity
+    int max_span = 1;
+    if (win_nodes(g, i, 0, mt - 1, rho_cut) <= cap_nodes) {
+        max_span = mt;
+    } else {
+        int lo = 1, hi = mt - 1;  // win_nodes(span lo) assumed to fit (else one-cell tiles go via L2)
+        while (lo < hi) {
+            int mid = (lo + hi + 1) / 2;
+            if (win_nodes(g, i, 0, mid - 1, rho_cut) <= cap_nodes) lo = mid; else hi = mid - 1;
+        }
+        max_span = lo;
+    }
     long long cur = 0, tstart = offset[(long long)ig * g.P];
     int c0 = 0;
     auto emit = [&](int a, int b, long long s0, long long s1) {
@@ -1029,7 +1079,7 @@ __device__ __forceinline__ int ring_tiles(const Geo& g, int i, const unsigned* o
         long long ce = offset[(long long)(ig + c + 1) * g.P];
         long long cnt = ce - cs;
         if (cnt == 0) continue;
-        if (cur > 0 && (cur + cnt > tile_max || win_nodes(g, i, c0, c, rho_cut) > cap_nodes)) {
+        if (cur > 0 && (cur + cnt > tile_max || c - c0 + 1 > max_span)) {
             emit(c0, c - 1 < c0 ? c0 : c - 1, tstart, cs);
             cur = 0;
             tstart = cs;
