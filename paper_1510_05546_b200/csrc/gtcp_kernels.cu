@@ -402,7 +402,8 @@ __global__ void __launch_bounds__(kDepositThreads, 3)
         unsigned long long fb = 0;
         long long clamps = 0;
         for (long long p = T.start + threadIdx.x; p < T.end; p += blockDim.x) {
-            const double psi = s.x[0][p], theta = s.x[1][p], zeta = s.x[2][p], w = s.x[4][p], mu = s.mu[p];
+            const double psi = __ldcs(s.x[0] + p), theta = __ldcs(s.x[1] + p), zeta = __ldcs(s.x[2] + p),
+                         w = __ldcs(s.x[4] + p), mu = __ldcs(s.mu + p);
             double r, invB, rho, inv_r;
             gyro_radius(g, psi, cos(theta), mu, &r, &invB, &rho, &inv_r);
             double wz1;
@@ -551,6 +552,23 @@ void launch_fx_to_real(const Geo& g, const long long* fx, double* rho, const Dev
 // gfield layout: interval k, node n -> 6 doubles (plane k: gr gth gpar,
 // plane k+1: gr gth gpar); label nodes j, j+1 are 96 contiguous bytes.
 // ---------------------------------------------------------------------------
+// per-ring geometry in shared memory (one 16-byte record per ring)
+struct RingTab {
+    double qtinv;
+    int mtheta, igrid;
+};
+
+__device__ __forceinline__ void load_ring_tab(const Geo& g, RingTab* rt) {
+    for (int i = threadIdx.x; i <= g.mpsi; i += blockDim.x) {
+        RingTab t;
+        t.qtinv = g.qtinv[i];
+        t.mtheta = g.mtheta[i];
+        t.igrid = g.igrid[i];
+        rt[i] = t;
+    }
+    __syncthreads();
+}
+
 struct PushPtrs {
     const double* src[5];
     const double* base[5];
@@ -566,9 +584,9 @@ __device__ __forceinline__ double warp_max(double v) {
 // One RK2 stage of one particle (U-1..U-8): returns the new state X[5] from
 // the source state (psi, theta, zeta, rho_par, w), mu and the base state.
 // Counts reflections / plane clamps into the caller's registers.
-__device__ __forceinline__ void push_one(const Geo& g, double psi, double theta, double zeta, double rho_par,
-                                         double w, double mu, const double* base, double h,
-                                         const double* __restrict__ gf, double* X, long long& refl,
+__device__ __forceinline__ void push_one(const Geo& g, const RingTab* __restrict__ rt, double psi, double theta,
+                                         double zeta, double rho_par, double w, double mu, const double* base,
+                                         double h, const double* __restrict__ gf, double* X, long long& refl,
                                          long long& clamps) {
     // U-1
     double st, ct;
@@ -586,15 +604,47 @@ __device__ __forceinline__ void push_one(const Geo& g, double psi, double theta,
     int k = kg - g.k0;
     if (k < 0 || k > g.P - 1) { clamps++; k = min(max(k, 0), g.P - 1); }
     const double wz0 = 1.0 - wz1;
-    // accumulate each bounding plane separately (4 FMA per component and
-    // (point, ring)); the plane weights and the 1/4 per gyro-point are applied
-    // once at the end.  a0/a1 carry 1/4 already (gyro_stencil), so use 4*a.
+    // phase 1: the 8 (gyro-point, ring) stencil records (ring tables in smem)
+    int node[8];
+    double wa[8], wb[8];
+    {
+        const double rho_r = rho * inv_r;
+#pragma unroll
+        for (int l = 0; l < 4; l++) {
+            double rl = r, tl = theta;
+            if (l == 0) rl = r + rho;
+            if (l == 2) rl = r - rho;
+            if (l == 1) tl = theta + rho_r;
+            if (l == 3) tl = theta - rho_r;
+            rl = fmin(fmax(rl, g.a0), g.a1);
+            const double x = (rl - g.a0) * g.inv_dr;
+            const int i = min(max((int)floor(x), 0), g.mpsi - 1);
+            const double wp1 = x - (double)i;
+#pragma unroll
+            for (int mm = 0; mm < 2; mm++) {
+                const RingTab t = rt[i + mm];
+                double s = (tl - zeta * t.qtinv) * kInvTwoPi;
+                s = s - floor(s);
+                s = s * (double)t.mtheta;
+                const int j = min((int)floor(s), t.mtheta - 1);
+                const double wt1 = s - (double)j;
+                const double wp = mm ? wp1 : 1.0 - wp1;
+                node[2 * l + mm] = t.igrid + j;
+                wa[2 * l + mm] = wp * (1.0 - wt1);
+                wb[2 * l + mm] = wp * wt1;
+            }
+        }
+    }
+    // phase 2: 8 x 96 contiguous bytes of the interval-interleaved field; each
+    // bounding plane accumulated separately, plane weights and 1/4 applied once
     double r0 = 0.0, t0 = 0.0, p0 = 0.0, r1 = 0.0, t1 = 0.0, p1 = 0.0;
     const double* gk = gf + (long long)k * g.mgrid * 6;
-    gyro_stencil(g, r, theta, zeta, rho, inv_r, [&](int m, int j, int mt, double a0, double a1) {
-        const double2* qq = reinterpret_cast<const double2*>(gk + ((long long)__ldg(g.igrid + m) + j) * 6);
-        double2 v0 = __ldg(qq + 0), v1 = __ldg(qq + 1), v2 = __ldg(qq + 2);
-        double2 v3 = __ldg(qq + 3), v4 = __ldg(qq + 4), v5 = __ldg(qq + 5);
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        const double2* qq = reinterpret_cast<const double2*>(gk + (long long)node[q] * 6);
+        const double2 v0 = __ldg(qq + 0), v1 = __ldg(qq + 1), v2 = __ldg(qq + 2);
+        const double2 v3 = __ldg(qq + 3), v4 = __ldg(qq + 4), v5 = __ldg(qq + 5);
+        const double a0 = wa[q], a1 = wb[q];
         // node j: (v0.x v0.y v1.x) plane k, (v1.y v2.x v2.y) plane k+1; node j+1 likewise in v3..v5
         r0 = fma(a0, v0.x, fma(a1, v3.x, r0));
         t0 = fma(a0, v0.y, fma(a1, v3.y, t0));
@@ -602,9 +652,9 @@ __device__ __forceinline__ void push_one(const Geo& g, double psi, double theta,
         r1 = fma(a0, v1.y, fma(a1, v4.y, r1));
         t1 = fma(a0, v2.x, fma(a1, v5.x, t1));
         p1 = fma(a0, v2.y, fma(a1, v5.y, p1));
-        (void)mt;
-    });
-    const double gr = wz0 * r0 + wz1 * r1, gt = wz0 * t0 + wz1 * t1, gp = wz0 * p0 + wz1 * p1;
+    }
+    const double wz0q = 0.25 * wz0, wz1q = 0.25 * wz1;
+    const double gr = wz0q * r0 + wz1q * r1, gt = wz0q * t0 + wz1q * t1, gp = wz0q * p0 + wz1q * p1;
     // U-3 drifts
     const double vpar = g.omega0 * B * rho_par;
     const double iOB = g.inv_omega0 * invB;  // 1 / (omega0 B)
@@ -671,22 +721,29 @@ __device__ __forceinline__ void push_epilogue(DevCounters* dc, double wmax, long
     if (nonfinite) dc->nonfinite = 1;
 }
 
-template <int MINB>
+template <int MINB, bool CS>
 __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long long n, double h,
                                              const double* __restrict__ gf, DevCounters* dc) {
+    extern __shared__ RingTab rt_dyn[];
+    load_ring_tab(g, rt_dyn);
     double wmax = 0.0;
     long long refl = 0, clamps = 0;
     int nonfinite = 0;
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
          p += (long long)gridDim.x * blockDim.x) {
+        // CS: particle streams evict-first (.cs) so they do not push the field out of L2
+        auto ld = [&](const double* a) { return CS ? __ldcs(a + p) : a[p]; };
         double base[5], X[5];
 #pragma unroll
-        for (int d = 0; d < 5; d++) base[d] = pp.base[d][p];
-        push_one(g, pp.src[0][p], pp.src[1][p], pp.src[2][p], pp.src[3][p], pp.src[4][p], pp.mu[p], base, h, gf,
-                 X, refl, clamps);
+        for (int d = 0; d < 5; d++) base[d] = ld(pp.base[d]);
+        push_one(g, rt_dyn, ld(pp.src[0]), ld(pp.src[1]), ld(pp.src[2]), ld(pp.src[3]), ld(pp.src[4]), ld(pp.mu),
+                 base, h, gf, X, refl, clamps);
         if (!(isfinite(X[0]) && isfinite(X[1]) && isfinite(X[2]) && isfinite(X[3]) && isfinite(X[4]))) nonfinite = 1;
 #pragma unroll
-        for (int d = 0; d < 5; d++) pp.out[d][p] = X[d];
+        for (int d = 0; d < 5; d++) {
+            if (CS) __stcs(pp.out[d] + p, X[d]);
+            else pp.out[d][p] = X[d];
+        }
         wmax = fmax(wmax, fabs(X[4]));
     }
     push_epilogue(dc, wmax, refl, clamps, nonfinite);
@@ -725,8 +782,10 @@ template <int NARR>
 __global__ void __launch_bounds__(kPC, 2) k_push_tma(Geo g, PushPtrs pp, long long n, double h,
                                                      const double* __restrict__ gf, DevCounters* dc) {
     // NARR = 6: src 5 + mu (stage 1, base == src); NARR = 11: + base 5 (stage 2)
-    extern __shared__ __align__(128) double sbuf[];  // [kNB][NARR][kPC]
+    extern __shared__ __align__(128) double sbuf[];  // [kNB][NARR][kPC], then the ring table
     __shared__ __align__(8) unsigned long long full[kNB];
+    RingTab* rt = reinterpret_cast<RingTab*>(sbuf + (size_t)kNB * NARR * kPC);
+    load_ring_tab(g, rt);
     const long long nchunks = (n + kPC - 1) / kPC;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kNB; s++) mbar_init(&full[s], 1);
@@ -764,7 +823,7 @@ __global__ void __launch_bounds__(kPC, 2) k_push_tma(Geo g, PushPtrs pp, long lo
             double base[5], X[5];
 #pragma unroll
             for (int d = 0; d < 5; d++) base[d] = (NARR == 11) ? sb[(6 + d) * kPC + t] : sb[d * kPC + t];
-            push_one(g, sb[0 * kPC + t], sb[1 * kPC + t], sb[2 * kPC + t], sb[3 * kPC + t], sb[4 * kPC + t],
+            push_one(g, rt, sb[0 * kPC + t], sb[1 * kPC + t], sb[2 * kPC + t], sb[3 * kPC + t], sb[4 * kPC + t],
                      sb[5 * kPC + t], base, h, gf, X, refl, clamps);
             if (!(isfinite(X[0]) && isfinite(X[1]) && isfinite(X[2]) && isfinite(X[3]) && isfinite(X[4])))
                 nonfinite = 1;
@@ -794,7 +853,7 @@ void launch_push3(const Geo& g, const double* const src[5], const double* const 
     pp.mu = mu;
     static int variant = [] {
         const char* e = getenv("GTCP_PUSH_VARIANT");
-        return e ? atoi(e) : 2;
+        return e ? atoi(e) : 4;
     }();
     const bool stage2 = (base[0] != src[0]);
     if (variant == 0) {
@@ -804,13 +863,13 @@ void launch_push3(const Geo& g, const double* const src[5], const double* const 
         long long nch = (n + kPC - 1) / kPC;
         int blocks = (int)std::min<long long>(nch, 2LL * nsm);
         if (stage2) {
-            size_t sm = (size_t)kNB * 11 * kPC * sizeof(double);
+            size_t sm = (size_t)kNB * 11 * kPC * sizeof(double) + (g.mpsi + 1) * sizeof(RingTab);
             static bool cfg = (cudaFuncSetAttribute(k_push_tma<11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     (int)sm) == cudaSuccess);
             (void)cfg;
             k_push_tma<11><<<blocks, kPC, sm, st>>>(g, pp, n, h, gfield, dc);
         } else {
-            size_t sm = (size_t)kNB * 6 * kPC * sizeof(double);
+            size_t sm = (size_t)kNB * 6 * kPC * sizeof(double) + (g.mpsi + 1) * sizeof(RingTab);
             static bool cfg = (cudaFuncSetAttribute(k_push_tma<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     (int)sm) == cudaSuccess);
             (void)cfg;
@@ -818,8 +877,10 @@ void launch_push3(const Geo& g, const double* const src[5], const double* const 
         }
     } else {
         int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
-        if (variant == 3) k_push<3><<<blocks, 256, 0, st>>>(g, pp, n, h, gfield, dc);
-        else k_push<2><<<blocks, 256, 0, st>>>(g, pp, n, h, gfield, dc);
+        size_t smr = (g.mpsi + 1) * sizeof(RingTab);
+        if (variant == 3) k_push<3, false><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
+        else if (variant == 4) k_push<2, true><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
+        else k_push<2, false><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
     }
     g_launches++;
 }

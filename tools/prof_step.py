@@ -24,7 +24,8 @@ import paper_1510_05546_b200 as G  # noqa: E402
 
 torch.cuda.set_device(0)
 over = {"micell": a.micell} if a.micell else {}
-ctx = G.Context(G.gtcp_default_params(a.size, bin_every=a.bin_every, **over))
+stream = torch.cuda.Stream()
+ctx = G.Context(G.gtcp_default_params(a.size, bin_every=a.bin_every, **over), stream=stream.cuda_stream)
 ctx.set_charge_mode(a.charge_mode)
 ctx.load()
 ctx.step(a.warmup)
