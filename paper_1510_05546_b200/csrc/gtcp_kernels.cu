@@ -413,6 +413,13 @@ __global__ void __launch_bounds__(kDepositThreads, 3)
             const double ws = __dmul_rn(w, scale);
             const double wzl = __dmul_rn(__dsub_rn(1.0, wz1), ws), wzu = __dmul_rn(wz1, ws);
             const double rho_r = __dmul_rn(rho, inv_r);
+            // lane-rotated plane order, fixed for the whole particle: pass A uses
+            // plane k + b3, pass B plane k + 1 - b3
+            const int kA = k + b3, kB = k + 1 - b3;
+            const double wzA = b3 ? wzu : wzl, wzB = b3 ? wzl : wzu;
+            const int* jsA = js + kA * kMaxRings;
+            const int* jsB = js + kB * kMaxRings;
+            const int baseA = kA * S, baseB = kB * S;
 #pragma unroll
             for (int lq = 0; lq < 4; lq++) {
                 // lane-rotated gyro-point: l = (lq + lane) mod 4.  r +- rho and
@@ -441,43 +448,33 @@ __global__ void __launch_bounds__(kDepositThreads, 3)
                     const double wp = mm ? wp1 : __dsub_rn(1.0, wp1);
                     const double a0 = __dmul_rn(__dmul_rn(0.25, wp), __dsub_rn(1.0, wt1));
                     const double a1 = __dmul_rn(__dmul_rn(0.25, wp), wt1);
+                    const int j1 = (j + 1 == mt) ? 0 : j + 1;
+                    // node order rotated by lane bit 4: first node ja (weight aa), then jb
+                    const int ja = b4 ? j1 : j, jb = b4 ? j : j1;
+                    const double aa = b4 ? a1 : a0, ab = b4 ? a0 : a1;
                     const int q = m - m_lo;
                     const bool inr = (unsigned)q < (unsigned)nr;
                     const int qc = inr ? q : 0;
                     const int2 wo = T.WO[qc];
                     const int W = inr ? wo.x : 0;
-                    const int j1 = (j + 1 == mt) ? 0 : j + 1;
-                    // node order j / j+1 rotated by lane bit 4
-                    const int ja = b4 ? j1 : j, jb = b4 ? j : j1;
-                    const double aa = b4 ? a1 : a0, ab = b4 ? a0 : a1;
 #pragma unroll
                     for (int kq = 0; kq < 2; kq++) {
-                        const int kk = kq ^ b3;  // lane-rotated plane choice
-                        const int kp = k + kk;
-                        const double wzk = kk ? wzu : wzl;
-                        int d = j - js[kp * kMaxRings + qc];
-                        d += (d < 0) ? mt : 0;
-                        d = inr ? d : 0;  // outside the band: js belongs to another ring (W = 0 anyway)
-                        const int d1 = (d + 1 == mt) ? 0 : d + 1;
-                        const int da = b4 ? d1 : d, db = b4 ? d : d1;
+                        const int jsv = (kq ? jsB : jsA)[qc];
+                        int da = ja - jsv, db = jb - jsv;
+                        da += (da < 0) ? mt : 0;
+                        db += (db < 0) ? mt : 0;
+                        const double wzk = kq ? wzB : wzA;
                         const double ta = fx_magic(wzk, aa), tb = fx_magic(wzk, ab);
-                        const bool oka = da < W, okb = db < W;
-                        const int base = kp * S + wo.y;
+                        // unsigned compare: outside the band jsv belongs to another ring and d may be negative
+                        const bool oka = (unsigned)da < (unsigned)W, okb = (unsigned)db < (unsigned)W;
+                        const int base = (kq ? baseB : baseA) + wo.y;
                         const int sa = oka ? base + da : trash, sb = okb ? base + db : trash;
-#ifdef GTCP_DEBUG
-                        if (!(sa >= 0 && sa <= trash && sb >= 0 && sb <= trash))
-                            printf("BAD slot sa=%d sb=%d da=%d db=%d d=%d j=%d mt=%d js=%d W=%d base=%d kp=%d q=%d nr=%d S=%d "
-                                   "total=%d cap=%d m=%d mlo=%d sl=%g zeta=%g theta=%g psi=%g tile=%d\n",
-                                   sa, sb, da, db, d, j, mt, js[kp * kMaxRings + qc], W, base, kp, q, nr, S, T.total,
-                                   cap_nodes, m, m_lo, sl, zeta, theta, psi, t);
-#endif
-                        DCHECK(sa >= 0 && sa <= trash && sb >= 0 && sb <= trash);
-                        DCHECK(kp * kMaxRings + qc < P1 * kMaxRings && kp >= 0);
                         atomicAdd(slo + sa, fx_lo(ta));
                         atomicAdd(shi + sa, fx_hi(ta));
                         atomicAdd(slo + sb, fx_lo(tb));
                         atomicAdd(shi + sb, fx_hi(tb));
                         if (__builtin_expect(!(oka && okb), 0)) {
+                            const int kp = kq ? kB : kA;
                             if (!oka) { long long v = fx_val(ta); if (v) { red_i64(fx + fx_node(g, kp, m, ja, mt), v); fb++; } }
                             if (!okb) { long long v = fx_val(tb); if (v) { red_i64(fx + fx_node(g, kp, m, jb, mt), v); fb++; } }
                         }
