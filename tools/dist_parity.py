@@ -27,6 +27,7 @@ ap.add_argument("--nparts", type=int, default=0, help="markers (0 = micell*(mgri
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--w-amp", type=float, default=None)
 ap.add_argument("--mzetamax", type=int, default=None)
+ap.add_argument("--npartdom", type=int, default=1)
 a = ap.parse_args()
 
 rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
@@ -36,14 +37,17 @@ import paper_1510_05546_b200 as G  # noqa: E402
 
 over = {"mzetamax": a.mzetamax} if a.mzetamax else {}
 cfg = synth.config(a.size, **over)
-params = G.gtcp_default_params(a.size, ntoroidal=world, track_ids=1, bin_every=1, **over)
+npd = a.npartdom
+ntor = world // npd
+rank_t, rank_p = rank // npd, rank % npd
+params = G.gtcp_default_params(a.size, ntoroidal=ntor, npartdom=npd, track_ids=1, bin_every=1, **over)
 geo = G.gtcp_geometry(params)
 n = a.nparts or cfg["micell"] * (geo["mgrid"] - cfg["mpsi"]) * cfg["mzetamax"]
 parts = synth.load_particles(cfg, n, seed=1, w_amp=a.w_amp)
-P = cfg["mzetamax"] // world
+P = cfg["mzetamax"] // ntor
 cz = cfg["mzetamax"] / (2.0 * math.pi)
 kg = np.minimum(np.floor(parts["zeta"] * cz).astype(np.int64), cfg["mzetamax"] - 1)
-mine = (kg // P) == rank
+mine = ((kg // P) == rank_t) & ((parts["id"] % npd) == rank_p)
 obj = [G.gtcp_nccl_unique_id() if rank == 0 else None]
 dist.broadcast_object_list(obj, src=0)
 ctx = G.Context(params, rank, world, obj[0])
@@ -101,12 +105,13 @@ for step in range(a.steps):
         owner_ok = True
         for r, x in enumerate(allp):
             kk = np.minimum(np.floor(x["zeta"] * cz).astype(np.int64), cfg["mzetamax"] - 1)
-            owner_ok &= bool(np.all(kk // P == r))
+            owner_ok &= bool(np.all(kk // P == r // npd))
         err["owner"] = int(owner_ok)
         # stage-1 charge on planes [r*P, r*P+P] of each rank vs the oracle's global grid
         ce = 0.0
         for r, g in enumerate(allrho):
-            ce = max(ce, float(np.max(np.abs(g[:P] - ch_ref[r * P:r * P + P]))))
+            t = r // npd  # every particle replica holds the full charge of its toroidal domain
+            ce = max(ce, float(np.max(np.abs(g[:P] - ch_ref[t * P:t * P + P]))))
         err["charge"] = ce / float(np.max(np.abs(ch_ref)))
         err["movers_sent"] = int(st["movers_sent"])
         report[f"step{step}"] = err
@@ -119,11 +124,11 @@ for step in range(a.steps):
     if rank != 0:
         orc_state = st_all
     zz = np.minimum(np.floor(st_all["zeta"] * cz).astype(np.int64), cfg["mzetamax"] - 1)
-    sel = (zz // P) == rank
+    sel = ((zz // P) == rank_t) & ((st_all["id"] % npd) == rank_p)
     ctx.set_particles({k: v[sel] for k, v in st_all.items()})
     ctx.set_grid(G.GRID_MARKER, nm)
 if rank == 0:
-    print(json.dumps({"world": world, "size": a.size, "n": int(n), "ok": bool(ok), **report}))
+    print(json.dumps({"world": world, "ntoroidal": ntor, "npartdom": npd, "size": a.size, "n": int(n), "ok": bool(ok), **report}))
 ctx.close()
 dist.destroy_process_group()
 sys.exit(0 if (rank != 0 or ok) else 1)
