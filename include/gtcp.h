@@ -77,7 +77,7 @@ typedef struct {
     /* decomposition: ntoroidal * npartdom == nranks */
     int32_t ntoroidal, npartdom;
     int32_t precision;      /* 64 (fp64 state and arithmetic)                  */
-    int32_t bin_every;      /* bin by cell every bin_every steps       */
+    int32_t bin_every;      /* bin by cell every bin_every steps; 2 */
     int32_t poisson_iters;  /* fixed weighted-Jacobi sweeps (F-2)              */
     int32_t paranl;         /* velocity-space nonlinearity on      */
     int32_t drifts;         /* 1; 0 = test-only drift-off flag                 */

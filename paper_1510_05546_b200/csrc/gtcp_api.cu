@@ -222,7 +222,7 @@ extern "C" gtcp_status gtcp_default_params(char size, gtcp_params* out) {
     memset(&p, 0, sizeof(p));
     p.mpsi = mpsi; p.mthetamax = mth; p.mzetamax = mze; p.micell = micell;
     p.ntoroidal = 1; p.npartdom = 1;
-    p.precision = 64; p.bin_every = 10; p.poisson_iters = 20; p.paranl = 1; p.drifts = 1; p.track_ids = 0;
+    p.precision = 64; p.bin_every = 2; p.poisson_iters = 20; p.paranl = 1; p.drifts = 1; p.track_ids = 0;
     p.a0 = 0.1; p.a1 = 0.9; p.R0 = 2.78; p.omega0 = 125.0 * mpsi / 90.0;
     p.q0 = 0.854; p.q2 = 2.184; p.rln = 2.2; p.rlt = 6.9; p.tau = 1.0; p.dt = 0.06;
     p.jacobi_omega = 1.0; p.w_init_amp = 1e-3; p.vcut = 5.0; p.capacity_factor = 1.0;
@@ -455,7 +455,8 @@ extern "C" void gtcp_destroy(gtcp_ctx c) {
     fold_pending(c);
     for (auto e : c->event_pool) cudaEventDestroy(e);
     auto F = [](void* p) { if (p) cudaFree(p); };
-    for (int d = 0; d < 5; d++) { F(c->bufA[d]); F(c->bufB[d]); }
+    // the live/saved/mu/scratch pointers are always a permutation of the original allocations
+    for (int d = 0; d < 5; d++) { F(c->live[d]); F(c->saved[d]); }
     F(c->mu); F(c->scratch); F(c->id); F(c->id_scratch);
     F(c->key); F(c->rankbuf); F(c->count); F(c->offset); F(c->scan_tmp); F(c->tiles);
     F(c->fx); F(c->rhoH); F(c->dnH); F(c->tmpH); F(c->phiH); F(c->rhs); F(c->jphi); F(c->g1); F(c->g2);
@@ -715,26 +716,35 @@ static gtcp_status do_bin(gtcp_ctx c) {
     launch_bin_dest(c->key, c->rankbuf, c->offset, c->n, c->rankbuf, c->st);
     // gather form: inv[dest[p]] = p once, then every array is written coalesced
     launch_perm_inverse(c->rankbuf, c->n, c->key, c->st);
-    // permute live state, mu (and the saved state when mid-step) with one scratch array
+    // permute live state, mu (and the saved state when mid-step) in one fused
+    // gather pass into the other ping-pong set + spare arrays, then swap pointers
     std::vector<double**> arrs;
     for (int d = 0; d < 5; d++) arrs.push_back(&c->live[d]);
     arrs.push_back(&c->mu);
     if (c->stage_next == 2)
         for (int d = 0; d < 5; d++) arrs.push_back(&c->saved[d]);
-    for (double** a : arrs) {
-        launch_gather_perm_f64(*a, c->scratch, c->key, c->n, c->st);
-        // keep bufA/bufB bookkeeping consistent: the scratch becomes the array
-        double* old = *a;
-        for (int d = 0; d < 5; d++) {
-            if (c->bufA[d] == old) c->bufA[d] = c->scratch;
-            if (c->bufB[d] == old) c->bufB[d] = c->scratch;
+    if (c->stage_next == 1) {
+        // saved[] is dead between steps: use it (and the scratch array) as destinations
+        const double* src[6];
+        double* dst[6];
+        for (int d = 0; d < 5; d++) { src[d] = c->live[d]; dst[d] = c->saved[d]; }
+        src[5] = c->mu;
+        dst[5] = c->scratch;
+        launch_gather_perm_multi(src, dst, 6, c->id, c->id ? c->id_scratch : nullptr, c->key, c->n, c->st);
+        for (int d = 0; d < 5; d++) std::swap(c->live[d], c->saved[d]);
+        std::swap(c->mu, c->scratch);
+        if (c->id) std::swap(c->id, c->id_scratch);
+    } else {
+        for (double** a : arrs) {
+            launch_gather_perm_f64(*a, c->scratch, c->key, c->n, c->st);
+            double* old = *a;
+            *a = c->scratch;
+            c->scratch = old;
         }
-        *a = c->scratch;
-        c->scratch = old;
-    }
-    if (c->id) {
-        launch_gather_perm_u64(c->id, c->id_scratch, c->key, c->n, c->st);
-        std::swap(c->id, c->id_scratch);
+        if (c->id) {
+            launch_gather_perm_u64(c->id, c->id_scratch, c->key, c->n, c->st);
+            std::swap(c->id, c->id_scratch);
+        }
     }
     launch_build_tiles(g, c->offset, c->tile_max, c->tiles, c->max_tiles, c->dc, c->dep_cap_nodes, c->st);
     c->n_binned = c->n;

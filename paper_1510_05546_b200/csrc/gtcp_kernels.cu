@@ -920,11 +920,22 @@ __device__ __forceinline__ unsigned bin_key(const Geo& g, double psi, double the
 
 __global__ void k_bin_keys(Geo g, PSet s, long long n, unsigned* __restrict__ key, unsigned* __restrict__ rank,
                            unsigned* __restrict__ count) {
-    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-         p += (long long)gridDim.x * blockDim.x) {
-        unsigned kk = bin_key(g, s.x[0][p], s.x[1][p], s.x[2][p]);
-        key[p] = kk;
-        rank[p] = atomicAdd(count + kk, 1u);
+    // cell-sorted input repeats a key ~100 times in a row: aggregate equal keys
+    // of a warp into one atomic (leader adds the group size, peers take offsets)
+    const int lane = threadIdx.x & 31;
+    for (long long p0 = (long long)blockIdx.x * blockDim.x; p0 < n; p0 += (long long)gridDim.x * blockDim.x) {
+        const long long p = p0 + threadIdx.x;
+        const bool act = p < n;
+        unsigned kk = act ? bin_key(g, s.x[0][p], s.x[1][p], s.x[2][p]) : 0xffffffffu;
+        const unsigned peers = __match_any_sync(0xffffffffu, kk);
+        const int leader = __ffs(peers) - 1;
+        unsigned base = 0;
+        if (act && lane == leader) base = atomicAdd(count + kk, (unsigned)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (act) {
+            key[p] = kk;
+            rank[p] = base + __popc(peers & ((1u << lane) - 1u));
+        }
     }
 }
 
@@ -1056,6 +1067,47 @@ __global__ void k_gather_perm(const T* __restrict__ src, T* __restrict__ dst, co
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         dst[i] = __ldg(src + inv[i]);
+}
+
+// all attribute arrays in one pass: dst_a[i] = src_a[inv[i]] for every a
+struct PermArrays {
+    const double* src[12];
+    double* dst[12];
+    int na;
+    const unsigned long long* id_src;
+    unsigned long long* id_dst;
+};
+
+__global__ void k_gather_perm_multi(PermArrays A, const unsigned* __restrict__ inv, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long s = inv[i];
+        double v[12];
+#pragma unroll
+        for (int a = 0; a < 12; a++)
+            if (a < A.na) v[a] = __ldg(A.src[a] + s);
+        unsigned long long id = A.id_src ? __ldg(A.id_src + s) : 0ull;
+#pragma unroll
+        for (int a = 0; a < 12; a++)
+            if (a < A.na) __stcs(A.dst[a] + i, v[a]);
+        if (A.id_src) A.id_dst[i] = id;
+    }
+}
+
+void launch_gather_perm_multi(const double* const* src, double* const* dst, int na, const unsigned long long* id_src,
+                              unsigned long long* id_dst, const unsigned* inv, long long n, cudaStream_t st) {
+    if (n <= 0) return;
+    PermArrays A;
+    for (int a = 0; a < 12; a++) {
+        A.src[a] = a < na ? src[a] : nullptr;
+        A.dst[a] = a < na ? dst[a] : nullptr;
+    }
+    A.na = na;
+    A.id_src = id_src;
+    A.id_dst = id_dst;
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    k_gather_perm_multi<<<blocks, 256, 0, st>>>(A, inv, n);
+    g_launches++;
 }
 
 void launch_gather_perm_f64(const double* src, double* dst, const unsigned* inv, long long n, cudaStream_t st) {
