@@ -1306,6 +1306,39 @@ __global__ void k_gather_perm_multi(PermArrays A, const unsigned* __restrict__ i
     }
 }
 
+// scatter form: dst_a[dest[p]] = src_a[p] (coalesced reads; on nearly sorted
+// input the writes come in runs)
+__global__ void k_scatter_perm_multi(PermArrays A, const unsigned* __restrict__ dest, long long n) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x) {
+        const long long d = dest[p];
+        double v[12];
+#pragma unroll
+        for (int a = 0; a < 12; a++)
+            if (a < A.na) v[a] = __ldcs(A.src[a] + p);
+#pragma unroll
+        for (int a = 0; a < 12; a++)
+            if (a < A.na) A.dst[a][d] = v[a];
+        if (A.id_src) A.id_dst[d] = A.id_src[p];
+    }
+}
+
+void launch_scatter_perm_multi(const double* const* src, double* const* dst, int na, const unsigned long long* id_src,
+                               unsigned long long* id_dst, const unsigned* dest, long long n, cudaStream_t st) {
+    if (n <= 0) return;
+    PermArrays A;
+    for (int a = 0; a < 12; a++) {
+        A.src[a] = a < na ? src[a] : nullptr;
+        A.dst[a] = a < na ? dst[a] : nullptr;
+    }
+    A.na = na;
+    A.id_src = id_src;
+    A.id_dst = id_dst;
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    k_scatter_perm_multi<<<blocks, 256, 0, st>>>(A, dest, n);
+    g_launches++;
+}
+
 void launch_gather_perm_multi(const double* const* src, double* const* dst, int na, const unsigned long long* id_src,
                               unsigned long long* id_dst, const unsigned* inv, long long n, cudaStream_t st) {
     if (n <= 0) return;
