@@ -74,8 +74,10 @@ enum gtcp_grid {
 typedef struct {
     /* grid and particle sizes (north_star gtcp_init arguments; Tab.2) */
     int32_t mpsi, mthetamax, mzetamax, micell;
-    /* decomposition: ntoroidal * npartdom == nranks */
-    int32_t ntoroidal, npartdom;
+    /* decomposition: ntoroidal * nradial * npartdom == nranks;
+     * rank = (toroidal * nradial + radial) * npartdom + particle replica.
+     * Radial domains: equal-area windows snapped to rings (G-6). */
+    int32_t ntoroidal, npartdom, nradial, reserved0;
     int32_t precision;      /* 64 (fp64 state and arithmetic)                  */
     int32_t bin_every;      /* bin by cell every bin_every steps; 2 */
     int32_t poisson_iters;  /* fixed weighted-Jacobi sweeps (F-2)              */
@@ -102,6 +104,9 @@ typedef struct {
     int32_t P;              /* local planes (mzetamax / ntoroidal)             */
     int32_t k0;             /* global index of local plane 0                   */
     int32_t rank_toroidal, rank_particle;
+    int32_t rank_radial;    /* radial domain of this rank                        */
+    int32_t ring_lo, ring_hi; /* owned gyrocentre radii [r(ring_lo), r(ring_hi)) */
+    int32_t reserved1;
     int64_t n_local;        /* particles currently owned by this rank          */
     int64_t capacity;       /* particle array capacity                         */
     int32_t stage_next;     /* 1 or 2: RK2 stage the next push expects         */
@@ -153,8 +158,9 @@ gtcp_status gtcp_geometry(const gtcp_params* p, int32_t* mtheta, int64_t* igrid,
 /* 128-byte NCCL unique id for rank 0 to broadcast (torch.distributed). */
 gtcp_status gtcp_nccl_unique_id(void* out128);
 
-/* Create a context for rank `rank` of `nranks` (nranks == ntoroidal*npartdom;
- * toroidal domain = rank / npartdom, particle replica = rank % npartdom).
+/* Create a context for rank `rank` of `nranks` (nranks ==
+ * ntoroidal*nradial*npartdom; toroidal domain = rank / (nradial*npartdom),
+ * radial domain = (rank / npartdom) % nradial, replica = rank % npartdom).
  * nccl_id: the 128-byte id from gtcp_nccl_unique_id, NULL iff nranks == 1.
  * cuda_stream: a cudaStream_t (NULL = legacy default stream) on which all work
  * is enqueued; the current CUDA device must be set by the caller.
@@ -174,7 +180,7 @@ gtcp_status gtcp_load(gtcp_ctx ctx);
 
 /* Upload n particles (host fp64 SoA): attr[GTCP_PSI..GTCP_MU] (6 arrays,
  * live state + mu); id may be NULL unless track_ids.  Particles must lie in
- * this rank's toroidal domain.  Recomputes the marker density from these
+ * this rank's toroidal (and radial) domain.  Recomputes the marker density from these
  * particles (collective over ranks) and bins.  ECAPACITY if n > capacity. */
 gtcp_status gtcp_set_particles(gtcp_ctx ctx, int64_t n, const double* const* attr, const uint64_t* id);
 
@@ -197,8 +203,9 @@ gtcp_status gtcp_field(gtcp_ctx ctx);
 /* stage 1: X0 <- X, X <- X + dt/2 F(X);  stage 2: X <- X0 + dt F(X) (U-7).
  * ESTATE if stage is not the one expected. */
 gtcp_status gtcp_push(gtcp_ctx ctx, int stage);
-/* Migrate particles to their owner domain (H-1, multi-hop with guard), then
- * bin by cell when the schedule says so (after stage 2 every bin_every steps). */
+/* Migrate particles to their owner domain (H-1 toroidal, then H-2 radial;
+ * multi-hop with guard), then bin by cell when the schedule says so (after
+ * stage 2 every bin_every steps). */
 gtcp_status gtcp_shift(gtcp_ctx ctx);
 /* Force a bin (cell sort, H-4) now. */
 gtcp_status gtcp_bin(gtcp_ctx ctx);

@@ -33,7 +33,8 @@ class GtcpError(RuntimeError):
 class Params(C.Structure):
     _fields_ = [
         ("mpsi", C.c_int32), ("mthetamax", C.c_int32), ("mzetamax", C.c_int32), ("micell", C.c_int32),
-        ("ntoroidal", C.c_int32), ("npartdom", C.c_int32), ("precision", C.c_int32), ("bin_every", C.c_int32),
+        ("ntoroidal", C.c_int32), ("npartdom", C.c_int32), ("nradial", C.c_int32), ("reserved0", C.c_int32),
+        ("precision", C.c_int32), ("bin_every", C.c_int32),
         ("poisson_iters", C.c_int32), ("paranl", C.c_int32), ("drifts", C.c_int32), ("track_ids", C.c_int32),
         ("a0", C.c_double), ("a1", C.c_double), ("R0", C.c_double), ("omega0", C.c_double),
         ("q0", C.c_double), ("q2", C.c_double), ("rln", C.c_double), ("rlt", C.c_double),
@@ -47,7 +48,8 @@ class Params(C.Structure):
 
 class Info(C.Structure):
     _fields_ = [("mgrid", C.c_int64), ("P", C.c_int32), ("k0", C.c_int32), ("rank_toroidal", C.c_int32),
-                ("rank_particle", C.c_int32), ("n_local", C.c_int64), ("capacity", C.c_int64),
+                ("rank_particle", C.c_int32), ("rank_radial", C.c_int32), ("ring_lo", C.c_int32),
+                ("ring_hi", C.c_int32), ("reserved1", C.c_int32), ("n_local", C.c_int64), ("capacity", C.c_int64),
                 ("stage_next", C.c_int32), ("steps_done", C.c_int32)]
 
 

@@ -18,7 +18,9 @@ using namespace gtcp;
 
 struct gtcp_ctx_s {
     gtcp_params prm;
-    int rank, nranks, rank_t, rank_p;
+    int rank, nranks, rank_t, rank_p, rank_r;
+    std::vector<int> rad_ring;    // radial window boundaries (ring indices), nradial+1
+    ncclComm_t sect = nullptr, rad = nullptr;  // same toroidal domain; same (toroidal, replica)
     cudaStream_t st;
     int device;
     ncclComm_t world = nullptr, tor = nullptr, part = nullptr;
@@ -221,7 +223,7 @@ extern "C" gtcp_status gtcp_default_params(char size, gtcp_params* out) {
     gtcp_params p;
     memset(&p, 0, sizeof(p));
     p.mpsi = mpsi; p.mthetamax = mth; p.mzetamax = mze; p.micell = micell;
-    p.ntoroidal = 1; p.npartdom = 1;
+    p.ntoroidal = 1; p.npartdom = 1; p.nradial = 1;
     p.precision = 64; p.bin_every = 2; p.poisson_iters = 20; p.paranl = 1; p.drifts = 1; p.track_ids = 0;
     p.a0 = 0.1; p.a1 = 0.9; p.R0 = 2.78; p.omega0 = 125.0 * mpsi / 90.0;
     p.q0 = 0.854; p.q2 = 2.184; p.rln = 2.2; p.rlt = 6.9; p.tau = 1.0; p.dt = 0.06;
@@ -269,15 +271,18 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     if (!p || !out || nranks < 1 || rank < 0 || rank >= nranks) return GTCP_EINVAL;
     if (p->precision != 64) return GTCP_EINVAL;
     if (p->mpsi < 2 || p->mthetamax < 4 || p->mzetamax < 2 || p->micell < 0) return GTCP_EINVAL;
-    if (p->ntoroidal < 1 || p->npartdom < 1) return GTCP_EINVAL;
-    if (p->mzetamax % p->ntoroidal != 0 || p->ntoroidal * p->npartdom != nranks) return GTCP_EINVARIANT;
+    const int nrad = p->nradial < 1 ? 1 : p->nradial;
+    if (p->ntoroidal < 1 || p->npartdom < 1 || nrad > 8) return GTCP_EINVAL;
+    if (p->mzetamax % p->ntoroidal != 0 || p->ntoroidal * nrad * p->npartdom != nranks) return GTCP_EINVARIANT;
     if (p->mzetamax / p->ntoroidal < 2) return GTCP_EINVARIANT;
     if (nranks > 1 && !nccl_id) return GTCP_EINVAL;
     gtcp_ctx c = new gtcp_ctx_s();
     c->prm = *p;
+    c->prm.nradial = nrad;
     c->rank = rank;
     c->nranks = nranks;
-    c->rank_t = rank / p->npartdom;
+    c->rank_t = rank / (nrad * p->npartdom);
+    c->rank_r = (rank / p->npartdom) % nrad;
     c->rank_p = rank % p->npartdom;
     c->st = (cudaStream_t)cuda_stream;
     cudaGetDevice(&c->device);
@@ -285,6 +290,15 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     c->mgrid = (int)build_geometry(p, c->mtheta, c->igrid, c->itran, c->qtinv);
     c->P = p->mzetamax / p->ntoroidal;
     c->k0 = c->rank_t * c->P;
+    // G-6: equal-area radial windows r_k = sqrt(a0^2 + (k/K)(a1^2 - a0^2)), snapped to the nearest ring
+    c->rad_ring.assign(nrad + 1, 0);
+    for (int kk = 0; kk <= nrad; kk++) {
+        double rk = std::sqrt(p->a0 * p->a0 + (double)kk / nrad * (p->a1 * p->a1 - p->a0 * p->a0));
+        int b = (int)std::floor((rk - p->a0) / ((p->a1 - p->a0) / p->mpsi) + 0.5);
+        c->rad_ring[kk] = std::min(std::max(b, 0), p->mpsi);
+    }
+    c->rad_ring[0] = 0;
+    c->rad_ring[nrad] = p->mpsi;
     const int M = p->mpsi, mg = c->mgrid, P = c->P;
     CU(dalloc(&c->d_mtheta, M + 1));
     CU(dalloc(&c->d_igrid, M + 2));
@@ -312,11 +326,24 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     g.rhoG = std::sqrt(2.0) / p->omega0;
     g.inv_omega0 = 1.0 / p->omega0;
     g.inv_omega0_R0 = 1.0 / (p->omega0 * p->R0);
+    g.nrad = nrad;
+    g.rank_r = c->rank_r;
+    for (int b = 0; b < 9; b++) g.rbound[b] = p->a1 + 1.0;
+    for (int b = 0; b <= nrad; b++) g.rbound[b] = p->a0 + c->rad_ring[b] * g.dr;
     g.mtheta = c->d_mtheta; g.igrid = c->d_igrid; g.itran = c->d_itran; g.qtinv = c->d_qtinv;
     g.node_ring = c->d_node_ring;
     // particle capacity: the loaded count plus headroom for shift imbalance
     long long per_plane = (long long)p->micell * (mg - M);
     long long n_load = per_plane * P / p->npartdom;
+    if (nrad > 1) {
+        // marker density ~ r (1 + r^2 / (2 R0^2)) (theta-average of J): share of this window
+        auto Mr = [&](double r) { return 0.5 * r * r + r * r * r * r / (8.0 * p->R0 * p->R0); };
+        double tot = Mr(p->a1) - Mr(p->a0);
+        double mx = 0.0;
+        for (int kk = 0; kk < nrad; kk++)
+            mx = std::max(mx, (Mr(p->a0 + c->rad_ring[kk + 1] * g.dr) - Mr(p->a0 + c->rad_ring[kk] * g.dr)) / tot);
+        n_load = (long long)std::ceil(per_plane * P * mx / p->npartdom);
+    }
     double headroom = nranks > 1 ? 0.10 : 0.0;
     c->cap = (long long)std::ceil(n_load * (p->capacity_factor + headroom)) + 1024;
     c->cap = (c->cap + 255) / 256 * 256;  // TMA-staged kernels copy whole 16-byte granules of 256-particle chunks
@@ -416,11 +443,14 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
         ncclUniqueId uid;
         memcpy(&uid, nccl_id, sizeof(uid));
         NC(ncclCommInitRank(&c->world, nranks, uid, rank));
-        NC(ncclCommSplit(c->world, c->rank_p, c->rank_t, &c->tor, nullptr));
-        NC(ncclCommSplit(c->world, c->rank_t, c->rank_p, &c->part, nullptr));
+        // toroidal ring: same (radial, replica); section: same toroidal domain;
+        // radial line: same (toroidal, replica)
+        NC(ncclCommSplit(c->world, c->rank_r * p->npartdom + c->rank_p, c->rank_t, &c->tor, nullptr));
+        NC(ncclCommSplit(c->world, c->rank_t, c->rank_r * p->npartdom + c->rank_p, &c->sect, nullptr));
+        NC(ncclCommSplit(c->world, c->rank_t * p->npartdom + c->rank_p, c->rank_r, &c->rad, nullptr));
     }
     // shift buffers (movers per stage ~1% at 8 domains; allocate generously)
-    if (p->ntoroidal > 1) {
+    if (p->ntoroidal > 1 || nrad > 1) {
         c->shift_cap = std::max<long long>(1 << 16, (long long)(0.08 * c->cap));
         for (int d = 0; d < 11; d++) {
             CU(dalloc(&c->sendL[d], c->shift_cap));
@@ -469,6 +499,8 @@ extern "C" void gtcp_destroy(gtcp_ctx c) {
     if (c->h_dc) cudaFreeHost(c->h_dc);
     if (c->h_scalar) cudaFreeHost(c->h_scalar);
     if (c->part) ncclCommDestroy(c->part);
+    if (c->sect) ncclCommDestroy(c->sect);
+    if (c->rad) ncclCommDestroy(c->rad);
     if (c->tor) ncclCommDestroy(c->tor);
     if (c->world) ncclCommDestroy(c->world);
     delete c;
@@ -483,6 +515,9 @@ extern "C" gtcp_status gtcp_info(gtcp_ctx c, gtcp_info_t* out) {
     out->k0 = c->k0;
     out->rank_toroidal = c->rank_t;
     out->rank_particle = c->rank_p;
+    out->rank_radial = c->rank_r;
+    out->ring_lo = c->rad_ring[c->rank_r];
+    out->ring_hi = c->rad_ring[c->rank_r + 1];
     out->n_local = c->n;
     out->capacity = c->cap;
     out->stage_next = c->stage_next;
@@ -579,8 +614,10 @@ static gtcp_status charge_reduce(gtcp_ctx c) {
         NC(ncclGroupEnd());
         launch_rotate_add_i64(g, c->fx_recv, c->fx, c->rank_t == 0 ? +1 : 0, c->st);
     }
-    if (c->prm.npartdom > 1) {
-        NC(ncclAllReduce(c->fx, c->fx, (size_t)P * mg, ncclInt64, ncclSum, c->part, c->st));
+    if (c->prm.npartdom * c->prm.nradial > 1) {
+        // particle replicas and radial domains of one toroidal domain hold partial
+        // charges of the same (replicated) grid: exact int64 sum
+        NC(ncclAllReduce(c->fx, c->fx, (size_t)P * mg, ncclInt64, ncclSum, c->sect, c->st));
     }
     launch_fx_to_real(g, c->fx, c->rhoH + mg, c->dc, P, c->st);
     launch_fill_dup(g, c->rhoH + mg, P, 1, c->st);
@@ -795,14 +832,19 @@ extern "C" gtcp_status gtcp_bin(gtcp_ctx c) {
 // ----------------------------------------------------------------------------
 // shift (H-1..H-3): implemented in gtcp_shift_host below
 // ----------------------------------------------------------------------------
-gtcp_status shift_exchange(gtcp_ctx c);
+gtcp_status shift_exchange(gtcp_ctx c, int dir);
 
 extern "C" gtcp_status gtcp_shift(gtcp_ctx c) {
     CHECK_CTX(c);
     {
         PhaseTimer t(c, GTCP_T_SHIFT);
+        // toroidal first, then radial (H-2)
         if (c->prm.ntoroidal > 1) {
-            gtcp_status s = shift_exchange(c);
+            gtcp_status s = shift_exchange(c, 0);
+            if (s != GTCP_OK) return s;
+        }
+        if (c->prm.nradial > 1) {
+            gtcp_status s = shift_exchange(c, 1);
             if (s != GTCP_OK) return s;
         }
     }
@@ -838,17 +880,36 @@ extern "C" gtcp_status gtcp_step(gtcp_ctx c, int nsteps) {
 extern "C" gtcp_status gtcp_load(gtcp_ctx c) {
     CHECK_CTX(c);
     const gtcp_params& p = c->prm;
-    long long per_plane = (long long)p.micell * (c->mgrid - p.mpsi);
-    long long n_dom = per_plane * c->P;
-    long long n = n_dom / p.npartdom + (c->rank_p < n_dom % p.npartdom ? 1 : 0);
+    const long long per_plane = (long long)p.micell * (c->mgrid - p.mpsi);
+    const long long n_dom = per_plane * c->P;
+    // radial windows take the share of the marker density r (1 + r^2/(2 R0^2))
+    // (theta-average of J) between their boundary rings
+    const double dr = (p.a1 - p.a0) / p.mpsi;
+    auto Mr = [&](double r) { return 0.5 * r * r + r * r * r * r / (8.0 * p.R0 * p.R0); };
+    const double tot = Mr(p.a1) - Mr(p.a0);
+    long long n_rad = n_dom, id_rad = 0;
+    if (p.nradial > 1) {
+        long long acc = 0;
+        for (int kk = 0; kk < p.nradial; kk++) {
+            long long nk = (kk == p.nradial - 1)
+                               ? n_dom - acc
+                               : (long long)std::floor(n_dom * (Mr(p.a0 + c->rad_ring[kk + 1] * dr) -
+                                                                 Mr(p.a0 + c->rad_ring[kk] * dr)) / tot);
+            if (kk == c->rank_r) { n_rad = nk; id_rad = acc; }
+            acc += nk;
+        }
+    }
+    const long long n = n_rad / p.npartdom + (c->rank_p < n_rad % p.npartdom ? 1 : 0);
     if (n > c->cap) return set_err(c, GTCP_ECAPACITY, "load: capacity");
-    long long id0 = (long long)c->rank_t * n_dom + (long long)c->rank_p * (n_dom / p.npartdom) +
-                    std::min<long long>(c->rank_p, n_dom % p.npartdom);
+    const long long id0 = (long long)c->rank_t * n_dom + id_rad + (long long)c->rank_p * (n_rad / p.npartdom) +
+                          std::min<long long>(c->rank_p, n_rad % p.npartdom);
     c->n = n;
     c->stage_next = 1;
     PSet s = live_set(c);
-    double zlo = c->k0 * (GTCP_TWO_PI / p.mzetamax), zhi = (c->k0 + c->P) * (GTCP_TWO_PI / p.mzetamax);
-    launch_load(c->geo, s, n, p.seed, id0, p.w_init_amp, p.vcut, zlo, zhi, c->st);
+    const double zlo = c->k0 * (GTCP_TWO_PI / p.mzetamax), zhi = (c->k0 + c->P) * (GTCP_TWO_PI / p.mzetamax);
+    const double rlo = p.a0 + c->rad_ring[c->rank_r] * dr;
+    const double rhi = (c->rank_r == p.nradial - 1) ? p.a1 : p.a0 + c->rad_ring[c->rank_r + 1] * dr;
+    launch_load(c->geo, s, n, p.seed, id0, p.w_init_amp, p.vcut, zlo, zhi, rlo, rhi, c->st);
     KCHECK();
     gtcp_status r = do_bin(c);
     if (r != GTCP_OK) return r;
@@ -1095,7 +1156,7 @@ extern "C" gtcp_status gtcp_set_charge_mode(gtcp_ctx c, int mode) {
 // ----------------------------------------------------------------------------
 // shift over NCCL (toroidal ring neighbours), H-1..H-3
 // ----------------------------------------------------------------------------
-gtcp_status shift_exchange(gtcp_ctx c) {
+gtcp_status shift_exchange(gtcp_ctx c, int dir) {
     static const bool prof = getenv("GTCP_PROFILE_SHIFT") != nullptr;
     cudaEvent_t ev[16];
     int nev = 0;
@@ -1108,8 +1169,12 @@ gtcp_status shift_exchange(gtcp_ctx c) {
     };
     mark();
     const Geo& g = c->geo;
-    const int nt = c->prm.ntoroidal;
-    const int left = (c->rank_t - 1 + nt) % nt, right = (c->rank_t + 1) % nt;
+    // dir 0: toroidal ring (periodic); dir 1: radial line (inner = left, outer = right)
+    const int nt = dir ? c->prm.nradial : c->prm.ntoroidal;
+    const int me = dir ? c->rank_r : c->rank_t;
+    ncclComm_t comm = dir ? c->rad : c->tor;
+    const int left = dir ? (me > 0 ? me - 1 : -1) : (me - 1 + nt) % nt;
+    const int right = dir ? (me < nt - 1 ? me + 1 : -1) : (me + 1) % nt;
     // movers carry the live state and mu, plus the saved RK2 state mid-step (H-3)
     const int nattr = (c->stage_next == 2) ? 11 : 6;
     long long start = 0;  // first pass scans everything, later passes only the arrivals
@@ -1129,20 +1194,21 @@ gtcp_status shift_exchange(gtcp_ctx c) {
         unsigned* offR = offL + (c->shift_blocks + 1);
         unsigned* offH = offR + (c->shift_blocks + 1);
         unsigned* offF = offH + (c->shift_blocks + 1);
-        launch_shift_classify(g, attrs[2], n, c->cls, cntL, cntR, c->st);
+        launch_shift_classify(g, attrs[2], attrs[0], dir, n, c->cls, cntL, cntR, c->st);
         launch_scan_u32(cntL, offL, nb, c->scan_tmp, c->st);
         launch_scan_u32(cntR, offR, nb, c->scan_tmp, c->st);
         launch_shift_nkeep(n, offL + nb, offR + nb, c->d_nkeep, c->d_counts, c->st);
         if (iter == 0) mark();
         // counts: mine (left, right) out; theirs in; global mover total
+        CU(cudaMemsetAsync(c->d_counts + 2, 0, 2 * sizeof(long long), c->st));
         NC(ncclGroupStart());
-        NC(ncclSend(c->d_counts + 0, 1, ncclInt64, left, c->tor, c->st));
-        NC(ncclSend(c->d_counts + 1, 1, ncclInt64, right, c->tor, c->st));
-        NC(ncclRecv(c->d_counts + 2, 1, ncclInt64, right, c->tor, c->st));  // right's left-movers
-        NC(ncclRecv(c->d_counts + 3, 1, ncclInt64, left, c->tor, c->st));   // left's right-movers
+        if (left >= 0) NC(ncclSend(c->d_counts + 0, 1, ncclInt64, left, comm, c->st));
+        if (right >= 0) NC(ncclSend(c->d_counts + 1, 1, ncclInt64, right, comm, c->st));
+        if (right >= 0) NC(ncclRecv(c->d_counts + 2, 1, ncclInt64, right, comm, c->st));  // right's left-movers
+        if (left >= 0) NC(ncclRecv(c->d_counts + 3, 1, ncclInt64, left, comm, c->st));    // left's right-movers
         NC(ncclGroupEnd());
         launch_sum_i64_pair(c->d_counts, c->d_counts + 4, c->st);
-        NC(ncclAllReduce(c->d_counts + 4, c->d_counts + 5, 1, ncclInt64, ncclSum, c->tor, c->st));
+        NC(ncclAllReduce(c->d_counts + 4, c->d_counts + 5, 1, ncclInt64, ncclSum, comm, c->st));
         CU(cudaMemcpyAsync(c->h_counts, c->d_counts, 6 * sizeof(long long), cudaMemcpyDeviceToHost, c->st));
         if (iter == 0) mark();
         CU(cudaStreamSynchronize(c->st));
@@ -1171,16 +1237,16 @@ gtcp_status shift_exchange(gtcp_ctx c) {
         // payload: straight into the particle arrays behind the keepers
         NC(ncclGroupStart());
         for (int d = 0; d < nattr; d++) {
-            NC(ncclSend(c->sendL[d], nL, ncclDouble, left, c->tor, c->st));
-            NC(ncclSend(c->sendR[d], nR, ncclDouble, right, c->tor, c->st));
-            NC(ncclRecv(attrs[d] + nkeep, rR, ncclDouble, right, c->tor, c->st));
-            NC(ncclRecv(attrs[d] + nkeep + rR, rL, ncclDouble, left, c->tor, c->st));
+            if (left >= 0) NC(ncclSend(c->sendL[d], nL, ncclDouble, left, comm, c->st));
+            if (right >= 0) NC(ncclSend(c->sendR[d], nR, ncclDouble, right, comm, c->st));
+            if (right >= 0) NC(ncclRecv(attrs[d] + nkeep, rR, ncclDouble, right, comm, c->st));
+            if (left >= 0) NC(ncclRecv(attrs[d] + nkeep + rR, rL, ncclDouble, left, comm, c->st));
         }
         if (idp) {
-            NC(ncclSend(c->sidL, nL, ncclUint64, left, c->tor, c->st));
-            NC(ncclSend(c->sidR, nR, ncclUint64, right, c->tor, c->st));
-            NC(ncclRecv(idp + nkeep, rR, ncclUint64, right, c->tor, c->st));
-            NC(ncclRecv(idp + nkeep + rR, rL, ncclUint64, left, c->tor, c->st));
+            if (left >= 0) NC(ncclSend(c->sidL, nL, ncclUint64, left, comm, c->st));
+            if (right >= 0) NC(ncclSend(c->sidR, nR, ncclUint64, right, comm, c->st));
+            if (right >= 0) NC(ncclRecv(idp + nkeep, rR, ncclUint64, right, comm, c->st));
+            if (left >= 0) NC(ncclRecv(idp + nkeep + rR, rL, ncclUint64, left, comm, c->st));
         }
         NC(ncclGroupEnd());
         if (iter == 0) mark();
@@ -1193,12 +1259,12 @@ gtcp_status shift_exchange(gtcp_ctx c) {
     // the fixed-point charge scale needs a bound on max|w| of the new particle
     // set: the max over the toroidal ranks is one (positive doubles order like
     // their uint64 bit patterns), no pass over the weights needed
-    NC(ncclAllReduce(&c->dc->wmax_bits, &c->dc->wmax_bits, 1, ncclUint64, ncclMax, c->tor, c->st));
+    NC(ncclAllReduce(&c->dc->wmax_bits, &c->dc->wmax_bits, 1, ncclUint64, ncclMax, comm, c->st));
     mark();
     KCHECK();
     if (prof) {
         cudaStreamSynchronize(c->st);
-        fprintf(stderr, "[shift r%d n=%lld]", c->rank, c->n);
+        fprintf(stderr, "[shift%d r%d n=%lld]", dir, c->rank, c->n);
         for (int i = 1; i < nev; i++) {
             float ms;
             cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);

@@ -16,6 +16,8 @@
 struct Geo {
     int mpsi, mzetamax, P, k0;     // rings, global planes, local planes, first local plane
     int ntor, rank_t;              // toroidal domains, this rank's toroidal index
+    int nrad, rank_r;              // radial domains, this rank's radial index
+    double rbound[9];              // radial domain boundaries r(b_0 = ring 0) .. r(b_nrad = ring mpsi)
     int mgrid;                     // nodes per plane incl. duplicates (< 2^31)
     int paranl, drifts;
     double a0, a1, dr, inv_dr, R0, inv_R0, omega0, q0, q2, rln, rlt, tau, dt;
@@ -97,7 +99,7 @@ void launch_permute_u64(const unsigned long long* src, unsigned long long* dst, 
 void launch_build_tiles(const Geo& g, const unsigned* offset, int tile_max, Tile* tiles, int max_tiles,
                         DevCounters* dc, int cap_nodes, cudaStream_t st);
 void launch_load(const Geo& g, const PSet& s, long long n, unsigned long long seed, long long id0,
-                 double w_amp, double vcut, double zlo, double zhi, cudaStream_t st);
+                 double w_amp, double vcut, double zlo, double zhi, double rlo, double rhi, cudaStream_t st);
 // grid kernels (gtcp_grid.cu)
 void launch_fill_dup(const Geo& g, double* f, int planes, int ncomp, cudaStream_t st);
 void launch_seam_rotate(const Geo& g, const double* src, double* dst, int shift_sign, cudaStream_t st);
@@ -125,8 +127,8 @@ void launch_sum_f64(const double* x, long long n, double* out, double* partial, 
 void launch_sum_i64_pair(const long long* in2, long long* out, cudaStream_t st);
 // shift (gtcp_shift.cu)
 int shift_chunks(long long n);
-void launch_shift_classify(const Geo& g, const double* zeta, long long n, unsigned char* cls, unsigned* cntL,
-                           unsigned* cntR, cudaStream_t st);
+void launch_shift_classify(const Geo& g, const double* zeta, const double* psi, int mode, long long n,
+                           unsigned char* cls, unsigned* cntL, unsigned* cntR, cudaStream_t st);
 void launch_shift_nkeep(long long n, const unsigned* totL, const unsigned* totR, long long* nkeep, long long* counts,
                         cudaStream_t st);
 void launch_shift_count_holes(const unsigned char* cls, long long n, const long long* nkeep, unsigned* cntH,

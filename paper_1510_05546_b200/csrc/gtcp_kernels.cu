@@ -1576,7 +1576,7 @@ struct Philox {
 };
 
 __global__ void k_load(Geo g, PSet s, long long n, unsigned long long seed, long long id0, double w_amp,
-                       double vcut, double zlo, double zhi) {
+                       double vcut, double zlo, double zhi, double rlo, double rhi) {
     const double jmax = (1.0 + g.a1 * g.inv_R0) * (1.0 + g.a1 * g.inv_R0);
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
          p += (long long)gridDim.x * blockDim.x) {
@@ -1589,7 +1589,8 @@ __global__ void k_load(Geo g, PSet s, long long n, unsigned long long seed, long
         rng.used = 4;
         double r, th;
         for (;;) {
-            r = sqrt(g.a0 * g.a0 + (g.a1 * g.a1 - g.a0 * g.a0) * rng.u53());
+            r = sqrt(rlo * rlo + (rhi * rhi - rlo * rlo) * rng.u53());
+            if (r >= rhi && rhi < g.a1) continue;  // radial window [rlo, rhi) (last window closed)
             th = GTCP_TWO_PI * rng.u53();
             double J = 1.0 + r * g.inv_R0 * cos(th);
             J *= J;
@@ -1618,10 +1619,10 @@ __global__ void k_load(Geo g, PSet s, long long n, unsigned long long seed, long
 }
 
 void launch_load(const Geo& g, const PSet& s, long long n, unsigned long long seed, long long id0, double w_amp,
-                 double vcut, double zlo, double zhi, cudaStream_t st) {
+                 double vcut, double zlo, double zhi, double rlo, double rhi, cudaStream_t st) {
     if (n <= 0) return;
     int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
-    k_load<<<blocks, 256, 0, st>>>(g, s, n, seed, id0, w_amp, vcut, zlo, zhi);
+    k_load<<<blocks, 256, 0, st>>>(g, s, n, seed, id0, w_amp, vcut, zlo, zhi, rlo, rhi);
     g_launches++;
 }
 

@@ -58,18 +58,31 @@ __device__ __forceinline__ long long warp_p(long long base, int it) {
     return base + (long long)(threadIdx.x >> 5) * kSub + it * 32 + (threadIdx.x & 31);
 }
 
-// classify: cls[p] in {0 keep, 1 left, 2 right}; per-chunk mover counts
-__global__ void __launch_bounds__(kShiftBlock) k_shift_classify(Geo g, const double* __restrict__ zeta, long long n,
+// H-2: radial domain of a gyrocentre radius r = sqrt(2 psi) (IEEE sqrt and
+// exact comparisons against the ring radii of the window boundaries)
+__device__ __forceinline__ int radial_domain(const Geo& g, double psi) {
+    const double r = sqrt(__dmul_rn(2.0, psi));
+    int d = 0;
+    for (int b = 1; b < g.nrad; b++) d += (r >= g.rbound[b]) ? 1 : 0;
+    return d;
+}
+
+// classify: cls[p] in {0 keep, 1 left, 2 right}; per-chunk mover counts.
+// mode 0: toroidal (periodic ring, the shorter way round); mode 1: radial
+// (inner = left, outer = right, not periodic)
+__global__ void __launch_bounds__(kShiftBlock) k_shift_classify(Geo g, const double* __restrict__ zeta,
+                                                                const double* __restrict__ psi, int mode, long long n,
                                                                 unsigned char* __restrict__ cls,
                                                                 unsigned* __restrict__ cntL,
                                                                 unsigned* __restrict__ cntR) {
     __shared__ unsigned sw[33];
     const long long base = (long long)blockIdx.x * kChunk;
+    const double* key = mode ? psi : zeta;
     double z[kIt];
 #pragma unroll
     for (int it = 0; it < kIt; it++) {
         long long p = warp_p(base, it);
-        z[it] = (p < n) ? __ldcs(zeta + p) : 0.0;
+        z[it] = (p < n) ? __ldcs(key + p) : 0.0;
     }
     unsigned a = 0, b = 0;
 #pragma unroll
@@ -77,10 +90,15 @@ __global__ void __launch_bounds__(kShiftBlock) k_shift_classify(Geo g, const dou
         long long p = warp_p(base, it);
         unsigned char c = 0;
         if (p < n) {
-            int d = shift_plane(g, z[it]) / g.P;
-            int rel = d - g.rank_t;
-            if (rel < 0) rel += g.ntor;
-            if (rel != 0) c = (rel <= g.ntor / 2) ? 2 : 1;
+            if (mode == 0) {
+                int d = shift_plane(g, z[it]) / g.P;
+                int rel = d - g.rank_t;
+                if (rel < 0) rel += g.ntor;
+                if (rel != 0) c = (rel <= g.ntor / 2) ? 2 : 1;
+            } else {
+                int rel = radial_domain(g, z[it]) - g.rank_r;
+                if (rel != 0) c = (rel > 0) ? 2 : 1;
+            }
             cls[p] = c;
         }
         a += __popc(__ballot_sync(0xffffffffu, c == 1));
@@ -256,10 +274,10 @@ __global__ void k_shift_nkeep(long long n, const unsigned* totL, const unsigned*
 int shift_chunks(long long n) { return (int)std::max<long long>(1, (n + kChunk - 1) / kChunk); }
 
 // ---------------------------------------------------------------------------
-void launch_shift_classify(const Geo& g, const double* zeta, long long n, unsigned char* cls, unsigned* cntL,
-                           unsigned* cntR, cudaStream_t st) {
+void launch_shift_classify(const Geo& g, const double* zeta, const double* psi, int mode, long long n,
+                           unsigned char* cls, unsigned* cntL, unsigned* cntR, cudaStream_t st) {
     int nb = shift_chunks(n);
-    k_shift_classify<<<nb, kShiftBlock, 0, st>>>(g, zeta, n, cls, cntL, cntR);
+    k_shift_classify<<<nb, kShiftBlock, 0, st>>>(g, zeta, psi, mode, n, cls, cntL, cntR);
     g_launches++;
 }
 

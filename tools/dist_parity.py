@@ -28,6 +28,7 @@ ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--w-amp", type=float, default=None)
 ap.add_argument("--mzetamax", type=int, default=None)
 ap.add_argument("--npartdom", type=int, default=1)
+ap.add_argument("--nradial", type=int, default=1)
 a = ap.parse_args()
 
 rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
@@ -37,17 +38,31 @@ import paper_1510_05546_b200 as G  # noqa: E402
 
 over = {"mzetamax": a.mzetamax} if a.mzetamax else {}
 cfg = synth.config(a.size, **over)
-npd = a.npartdom
-ntor = world // npd
-rank_t, rank_p = rank // npd, rank % npd
-params = G.gtcp_default_params(a.size, ntoroidal=ntor, npartdom=npd, track_ids=1, bin_every=1, **over)
+npd, nrad = a.npartdom, a.nradial
+ntor = world // (npd * nrad)
+rank_t, rank_r, rank_p = rank // (npd * nrad), (rank // npd) % nrad, rank % npd
+params = G.gtcp_default_params(a.size, ntoroidal=ntor, npartdom=npd, nradial=nrad, track_ids=1, bin_every=1, **over)
 geo = G.gtcp_geometry(params)
 n = a.nparts or cfg["micell"] * (geo["mgrid"] - cfg["mpsi"]) * cfg["mzetamax"]
 parts = synth.load_particles(cfg, n, seed=1, w_amp=a.w_amp)
 P = cfg["mzetamax"] // ntor
+# G-6 radial windows: equal-area split snapped to the nearest ring (test-side restatement)
+_dr = (cfg["a1"] - cfg["a0"]) / cfg["mpsi"]
+_rb = [0]
+for _k in range(1, nrad):
+    _rk = math.sqrt(cfg["a0"] ** 2 + _k / nrad * (cfg["a1"] ** 2 - cfg["a0"] ** 2))
+    _rb.append(min(max(int(math.floor((_rk - cfg["a0"]) / _dr + 0.5)), 0), cfg["mpsi"]))
+_rb.append(cfg["mpsi"])
+_rbound = np.array([cfg["a0"] + b * _dr for b in _rb])
+
+
+def rdom(psi):
+    r = np.sqrt(2.0 * psi)
+    return np.sum(r[:, None] >= _rbound[None, 1:nrad], axis=1) if nrad > 1 else np.zeros(len(psi), np.int64)
+
 cz = cfg["mzetamax"] / (2.0 * math.pi)
 kg = np.minimum(np.floor(parts["zeta"] * cz).astype(np.int64), cfg["mzetamax"] - 1)
-mine = ((kg // P) == rank_t) & ((parts["id"] % npd) == rank_p)
+mine = ((kg // P) == rank_t) & (rdom(parts["psi"]) == rank_r) & ((parts["id"] % npd) == rank_p)
 obj = [G.gtcp_nccl_unique_id() if rank == 0 else None]
 dist.broadcast_object_list(obj, src=0)
 ctx = G.Context(params, rank, world, obj[0])
@@ -105,12 +120,13 @@ for step in range(a.steps):
         owner_ok = True
         for r, x in enumerate(allp):
             kk = np.minimum(np.floor(x["zeta"] * cz).astype(np.int64), cfg["mzetamax"] - 1)
-            owner_ok &= bool(np.all(kk // P == r // npd))
+            owner_ok &= bool(np.all(kk // P == r // (npd * nrad)))
+            owner_ok &= bool(np.all(rdom(x["psi"]) == (r // npd) % nrad))
         err["owner"] = int(owner_ok)
         # stage-1 charge on planes [r*P, r*P+P] of each rank vs the oracle's global grid
         ce = 0.0
         for r, g in enumerate(allrho):
-            t = r // npd  # every particle replica holds the full charge of its toroidal domain
+            t = r // (npd * nrad)  # every replica / radial domain holds the full charge of its toroidal domain
             ce = max(ce, float(np.max(np.abs(g[:P] - ch_ref[t * P:t * P + P]))))
         err["charge"] = ce / float(np.max(np.abs(ch_ref)))
         err["movers_sent"] = int(st["movers_sent"])
@@ -124,11 +140,11 @@ for step in range(a.steps):
     if rank != 0:
         orc_state = st_all
     zz = np.minimum(np.floor(st_all["zeta"] * cz).astype(np.int64), cfg["mzetamax"] - 1)
-    sel = ((zz // P) == rank_t) & ((st_all["id"] % npd) == rank_p)
+    sel = ((zz // P) == rank_t) & (rdom(st_all["psi"]) == rank_r) & ((st_all["id"] % npd) == rank_p)
     ctx.set_particles({k: v[sel] for k, v in st_all.items()})
     ctx.set_grid(G.GRID_MARKER, nm)
 if rank == 0:
-    print(json.dumps({"world": world, "ntoroidal": ntor, "npartdom": npd, "size": a.size, "n": int(n), "ok": bool(ok), **report}))
+    print(json.dumps({"world": world, "ntoroidal": ntor, "nradial": nrad, "npartdom": npd, "size": a.size, "n": int(n), "ok": bool(ok), **report}))
 ctx.close()
 dist.destroy_process_group()
 sys.exit(0 if (rank != 0 or ok) else 1)
