@@ -78,7 +78,7 @@ typedef struct {
      * rank = (toroidal * nradial + radial) * npartdom + particle replica.
      * Radial domains: equal-area windows snapped to rings (G-6). */
     int32_t ntoroidal, npartdom, nradial, reserved0;
-    int32_t precision;      /* 64 (fp64 state and arithmetic)                  */
+    int32_t precision;      /* 64: fp64 state; 32: fp32 state (class D), fp64 arithmetic */
     int32_t bin_every;      /* bin by cell every bin_every steps; 2 */
     int32_t poisson_iters;  /* fixed weighted-Jacobi sweeps (F-2)              */
     int32_t paranl;         /* velocity-space nonlinearity on      */

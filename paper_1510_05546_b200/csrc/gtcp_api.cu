@@ -126,6 +126,7 @@ static gtcp_status set_err(gtcp_ctx c, gtcp_status s, const std::string& msg) {
     do {                                                                                           \
         if (!(c)) return GTCP_EINVAL;                                                              \
         if ((c)->sticky != GTCP_OK) return GTCP_ESTATE;                                            \
+        gtcp::g_prec32 = (c)->geo.prec32;                                                          \
     } while (0)
 #define KCHECK()                                                                                   \
     do {                                                                                           \
@@ -269,7 +270,7 @@ static cudaError_t dalloc(T** p, size_t count) {
 extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, const void* nccl_id,
                                  void* cuda_stream, gtcp_ctx* out) {
     if (!p || !out || nranks < 1 || rank < 0 || rank >= nranks) return GTCP_EINVAL;
-    if (p->precision != 64) return GTCP_EINVAL;
+    if (p->precision != 64 && p->precision != 32) return GTCP_EINVAL;
     if (p->mpsi < 2 || p->mthetamax < 4 || p->mzetamax < 2 || p->micell < 0) return GTCP_EINVAL;
     const int nrad = p->nradial < 1 ? 1 : p->nradial;
     if (p->ntoroidal < 1 || p->npartdom < 1 || nrad > 8) return GTCP_EINVAL;
@@ -318,6 +319,9 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     Geo& g = c->geo;
     g.mpsi = M; g.mzetamax = p->mzetamax; g.P = P; g.k0 = c->k0; g.ntor = p->ntoroidal; g.rank_t = c->rank_t;
     g.mgrid = mg; g.paranl = p->paranl; g.drifts = p->drifts;
+    g.prec32 = (p->precision == 32);
+    gtcp::g_prec32 = g.prec32;
+    const size_t es = g.prec32 ? sizeof(float) : sizeof(double);  // particle element size
     g.a0 = p->a0; g.a1 = p->a1; g.dr = (p->a1 - p->a0) / M; g.inv_dr = 1.0 / g.dr;
     g.R0 = p->R0; g.inv_R0 = 1.0 / p->R0; g.omega0 = p->omega0; g.q0 = p->q0; g.q2 = p->q2;
     g.rln = p->rln; g.rlt = p->rlt; g.tau = p->tau; g.dt = p->dt;
@@ -347,14 +351,16 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     double headroom = nranks > 1 ? 0.10 : 0.0;
     c->cap = (long long)std::ceil(n_load * (p->capacity_factor + headroom)) + 1024;
     c->cap = (c->cap + 255) / 256 * 256;  // TMA-staged kernels copy whole 16-byte granules of 256-particle chunks
+    // particle arrays hold `es`-byte reals (fp64 or fp32 state); typed double* for plumbing only
+    auto palloc = [&](double** ptr, long long count) { return cudaMalloc((void**)ptr, std::max<long long>(count, 1) * es); };
     for (int d = 0; d < 5; d++) {
-        CU(dalloc(&c->bufA[d], c->cap));
-        CU(dalloc(&c->bufB[d], c->cap));
+        CU(palloc(&c->bufA[d], c->cap));
+        CU(palloc(&c->bufB[d], c->cap));
         c->live[d] = c->bufA[d];
         c->saved[d] = c->bufB[d];
     }
-    CU(dalloc(&c->mu, c->cap));
-    CU(dalloc(&c->scratch, c->cap));
+    CU(palloc(&c->mu, c->cap));
+    CU(palloc(&c->scratch, c->cap));
     if (p->track_ids) {
         CU(dalloc(&c->id, c->cap));
         CU(dalloc(&c->id_scratch, c->cap));
@@ -453,8 +459,8 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     if (p->ntoroidal > 1 || nrad > 1) {
         c->shift_cap = std::max<long long>(1 << 16, (long long)(0.08 * c->cap));
         for (int d = 0; d < 11; d++) {
-            CU(dalloc(&c->sendL[d], c->shift_cap));
-            CU(dalloc(&c->sendR[d], c->shift_cap));
+            CU(palloc(&c->sendL[d], c->shift_cap));
+            CU(palloc(&c->sendR[d], c->shift_cap));
         }
         if (p->track_ids) {
             CU(dalloc(&c->sidL, c->shift_cap));
@@ -523,6 +529,32 @@ extern "C" gtcp_status gtcp_info(gtcp_ctx c, gtcp_info_t* out) {
     out->stage_next = c->stage_next;
     out->steps_done = c->steps_done;
     return GTCP_OK;
+}
+
+// host fp64 <-> device particle array (fp64, or fp32 state converted on the host)
+static cudaError_t upload_reals(gtcp_ctx c, double* dev, const double* host, long long n) {
+    if (n <= 0) return cudaSuccess;
+    if (!c->geo.prec32) return cudaMemcpyAsync(dev, host, n * sizeof(double), cudaMemcpyHostToDevice, c->st);
+    std::vector<float> tmp(host, host + n);
+    cudaError_t e = cudaMemcpyAsync(dev, tmp.data(), n * sizeof(float), cudaMemcpyHostToDevice, c->st);
+    if (e != cudaSuccess) return e;
+    return cudaStreamSynchronize(c->st);  // tmp dies here
+}
+
+static cudaError_t download_reals(gtcp_ctx c, double* host, const double* dev, long long n) {
+    if (n <= 0) return cudaSuccess;
+    if (!c->geo.prec32) return cudaMemcpyAsync(host, dev, n * sizeof(double), cudaMemcpyDeviceToHost, c->st);
+    std::vector<float> tmp(n);
+    cudaError_t e = cudaMemcpyAsync(tmp.data(), dev, n * sizeof(float), cudaMemcpyDeviceToHost, c->st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
+    if (e != cudaSuccess) return e;
+    for (long long i = 0; i < n; i++) host[i] = tmp[i];
+    return cudaSuccess;
+}
+
+// pointer to element `count` of a particle array of the context's element size
+static double* pofs(double* base, long long count) {
+    return reinterpret_cast<double*>(reinterpret_cast<char*>(base) + count * (gtcp::g_prec32 ? 4 : 8));
 }
 
 static PSet live_set(gtcp_ctx c) {
@@ -725,7 +757,7 @@ static void push_range(gtcp_ctx c, double* const* src, double* const* base, doub
         return e && e[0] == '1';
     }();
     long long tiled_end = 0;
-    if (tiled && c->charge_mode == 0 && c->n_binned > 0) {
+    if (tiled && !c->geo.prec32 && c->charge_mode == 0 && c->n_binned > 0) {
         tiled_end = std::min(c->n, c->n_binned);
         launch_push_tiled(c->geo, src, base, out, c->mu, tiled_end, h, c->gfield, c->tiles, c->dc, c->st);
     }
@@ -734,11 +766,11 @@ static void push_range(gtcp_ctx c, double* const* src, double* const* base, doub
         const double* b2[5];
         double* o2[5];
         for (int d = 0; d < 5; d++) {
-            s2[d] = src[d] + tiled_end;
-            b2[d] = base[d] + tiled_end;
-            o2[d] = out[d] + tiled_end;
+            s2[d] = pofs(src[d], tiled_end);
+            b2[d] = pofs(base[d], tiled_end);
+            o2[d] = pofs(out[d], tiled_end);
         }
-        launch_push3(c->geo, s2, b2, o2, c->mu + tiled_end, c->n - tiled_end, h, c->gfield, c->dc, c->st);
+        launch_push3(c->geo, s2, b2, o2, pofs(c->mu, tiled_end), c->n - tiled_end, h, c->gfield, c->dc, c->st);
     }
 }
 
@@ -926,9 +958,8 @@ extern "C" gtcp_status gtcp_set_particles(gtcp_ctx c, int64_t n, const double* c
     if (c->prm.track_ids && n > 0 && !id) return set_err(c, GTCP_EINVAL, "set_particles: ids required");
     for (int d = 0; d < 6; d++)
         if (n > 0 && !attr[d]) return set_err(c, GTCP_EINVAL, "set_particles: null attribute");
-    for (int d = 0; d < 5; d++)
-        CU(cudaMemcpyAsync(c->live[d], attr[d], n * sizeof(double), cudaMemcpyHostToDevice, c->st));
-    CU(cudaMemcpyAsync(c->mu, attr[5], n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    for (int d = 0; d < 5; d++) CU(upload_reals(c, c->live[d], attr[d], n));
+    CU(upload_reals(c, c->mu, attr[5], n));
     if (c->id && id) CU(cudaMemcpyAsync(c->id, id, n * sizeof(uint64_t), cudaMemcpyHostToDevice, c->st));
     c->n = n;
     c->stage_next = 1;
@@ -950,7 +981,7 @@ extern "C" gtcp_status gtcp_get_particles(gtcp_ctx c, int64_t cap, int64_t* n, d
         for (int d = 0; d < 5; d++) { src[d] = c->live[d]; src[6 + d] = c->saved[d]; }
         src[5] = c->mu;
         for (int d = 0; d < 11; d++)
-            if (attr[d]) CU(cudaMemcpyAsync(attr[d], src[d], c->n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+            if (attr[d]) CU(download_reals(c, attr[d], src[d], c->n));
     }
     if (id && c->id) CU(cudaMemcpyAsync(id, c->id, c->n * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
     CU(cudaStreamSynchronize(c->st));
@@ -993,16 +1024,14 @@ extern "C" gtcp_status gtcp_step_host(gtcp_ctx c, int64_t n, double* const* attr
     if (n < 0 || n > c->cap || !attr) return set_err(c, GTCP_EINVAL, "step_host: bad args");
     for (int d = 0; d < 6; d++)
         if (!attr[d]) return set_err(c, GTCP_EINVAL, "step_host: null attribute");
-    for (int d = 0; d < 5; d++)
-        CU(cudaMemcpyAsync(c->live[d], attr[d], n * sizeof(double), cudaMemcpyHostToDevice, c->st));
-    CU(cudaMemcpyAsync(c->mu, attr[5], n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    for (int d = 0; d < 5; d++) CU(upload_reals(c, c->live[d], attr[d], n));
+    CU(upload_reals(c, c->mu, attr[5], n));
     c->n = n;
     c->stage_next = 1;
     launch_wmax(c->live[4], c->n, c->dc, c->st);
     gtcp_status r = gtcp_step(c, nsteps);
     if (r != GTCP_OK) return r;
-    for (int d = 0; d < 5; d++)
-        CU(cudaMemcpyAsync(attr[d], c->live[d], c->n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    for (int d = 0; d < 5; d++) CU(download_reals(c, attr[d], c->live[d], c->n));
     CU(cudaStreamSynchronize(c->st));
     return GTCP_OK;
 }
@@ -1180,9 +1209,9 @@ gtcp_status shift_exchange(gtcp_ctx c, int dir) {
     long long start = 0;  // first pass scans everything, later passes only the arrivals
     for (int iter = 0; iter <= nt; iter++) {
         double* attrs[11];
-        for (int d = 0; d < 5; d++) attrs[d] = c->live[d] + start;
-        attrs[5] = c->mu + start;
-        for (int d = 0; d < 5; d++) attrs[6 + d] = c->saved[d] + start;
+        for (int d = 0; d < 5; d++) attrs[d] = pofs(c->live[d], start);
+        attrs[5] = pofs(c->mu, start);
+        for (int d = 0; d < 5; d++) attrs[6 + d] = pofs(c->saved[d], start);
         unsigned long long* idp = c->id ? c->id + start : nullptr;
         const long long n = c->n - start;
         const int nb = shift_chunks(n);
@@ -1237,10 +1266,11 @@ gtcp_status shift_exchange(gtcp_ctx c, int dir) {
         // payload: straight into the particle arrays behind the keepers
         NC(ncclGroupStart());
         for (int d = 0; d < nattr; d++) {
-            if (left >= 0) NC(ncclSend(c->sendL[d], nL, ncclDouble, left, comm, c->st));
-            if (right >= 0) NC(ncclSend(c->sendR[d], nR, ncclDouble, right, comm, c->st));
-            if (right >= 0) NC(ncclRecv(attrs[d] + nkeep, rR, ncclDouble, right, comm, c->st));
-            if (left >= 0) NC(ncclRecv(attrs[d] + nkeep + rR, rL, ncclDouble, left, comm, c->st));
+            const ncclDataType_t ty = g.prec32 ? ncclFloat : ncclDouble;
+            if (left >= 0) NC(ncclSend(c->sendL[d], nL, ty, left, comm, c->st));
+            if (right >= 0) NC(ncclSend(c->sendR[d], nR, ty, right, comm, c->st));
+            if (right >= 0) NC(ncclRecv(pofs(attrs[d], nkeep), rR, ty, right, comm, c->st));
+            if (left >= 0) NC(ncclRecv(pofs(attrs[d], nkeep + rR), rL, ty, left, comm, c->st));
         }
         if (idp) {
             if (left >= 0) NC(ncclSend(c->sidL, nL, ncclUint64, left, comm, c->st));

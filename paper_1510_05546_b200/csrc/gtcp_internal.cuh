@@ -20,6 +20,7 @@ struct Geo {
     double rbound[9];              // radial domain boundaries r(b_0 = ring 0) .. r(b_nrad = ring mpsi)
     int mgrid;                     // nodes per plane incl. duplicates (< 2^31)
     int paranl, drifts;
+    int prec32;                    // particle store in fp32 (arithmetic stays fp64)
     double a0, a1, dr, inv_dr, R0, inv_R0, omega0, q0, q2, rln, rlt, tau, dt;
     double cz;                     // mzetamax / (2 pi), rounded once (Q-2, H-1)
     double dzeta;                  // 2 pi / mzetamax
@@ -144,5 +145,6 @@ void launch_fill_f64(double* x, long long n, double v, cudaStream_t st);
 void launch_gather_f64(const double* src, const long long* idx, long long m, double* out, cudaStream_t st);
 
 extern long long g_launches;  // kernels launched (for the bench's gpu_launches claim)
+extern int g_prec32;          // precision of the current context's particle store
 
 }  // namespace gtcp

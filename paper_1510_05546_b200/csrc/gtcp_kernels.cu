@@ -30,6 +30,7 @@
 namespace gtcp {
 
 long long g_launches = 0;
+int g_prec32 = 0;  // precision of the particle store of the context being driven (set per call)
 
 static constexpr double kInvTwoPi = 1.0 / GTCP_TWO_PI;
 static constexpr int kMaxRings = 16;   // radial band of one tile window
@@ -178,6 +179,19 @@ __device__ __forceinline__ void smem_add(unsigned* lo, int* hi, int slot, long l
 
 __device__ __forceinline__ double fx_scale(const DevCounters* dc) { return scalbn(1.0, dc->fx_shift); }
 
+// particle storage of type R (double for precision 64, float for 32): the
+// arithmetic is always fp64 (fp32 state, fp64 index/weight math)
+template <class R>
+__device__ __forceinline__ double ldp(const double* a, long long p) { return (double)reinterpret_cast<const R*>(a)[p]; }
+template <class R>
+__device__ __forceinline__ double ldp_cs(const double* a, long long p) {
+    return (double)__ldcs(reinterpret_cast<const R*>(a) + p);
+}
+template <class R>
+__device__ __forceinline__ void stp(double* a, long long p, double v) { reinterpret_cast<R*>(a)[p] = (R)v; }
+template <class R>
+__device__ __forceinline__ void stp_cs(double* a, long long p, double v) { __stcs(reinterpret_cast<R*>(a) + p, (R)v); }
+
 // ---------------------------------------------------------------------------
 // charge: fixed-point scale.  F = 35 - e with max|w| in [2^(e-1), 2^e), so
 // |w| 2^F < 2^35 and every contribution (<= |w|/4) rounds to an integer of
@@ -207,13 +221,15 @@ void launch_fx_scale(DevCounters* dc, cudaStream_t st) {
 // Used for particles outside any tile (arrivals after a shift) and as the
 // reference mode 1.
 // ---------------------------------------------------------------------------
+template <class R>
 __global__ void __launch_bounds__(256) k_deposit_direct(Geo g, PSet s, long long begin, long long n,
                                                         long long* __restrict__ fx, DevCounters* dc) {
     const double scale = fx_scale(dc);
     long long clamps = 0;
     for (long long p = begin + blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
          p += (long long)gridDim.x * blockDim.x) {
-        double psi = s.x[0][p], theta = s.x[1][p], zeta = s.x[2][p], w = s.x[4][p], mu = s.mu[p];
+        double psi = ldp<R>(s.x[0], p), theta = ldp<R>(s.x[1], p), zeta = ldp<R>(s.x[2], p), w = ldp<R>(s.x[4], p),
+               mu = ldp<R>(s.mu, p);
         double r, invB, rho, inv_r;
         gyro_radius(g, psi, cos(theta), mu, &r, &invB, &rho, &inv_r);
         double wz1;
@@ -240,7 +256,8 @@ void launch_deposit_direct(const Geo& g, const PSet& s, long long begin, long lo
     if (n <= begin) return;
     long long work = n - begin;
     int blocks = (int)std::min<long long>((work + 255) / 256, 148LL * 16);
-    k_deposit_direct<<<blocks, 256, 0, st>>>(g, s, begin, n, fx, dc);
+    if (g.prec32) k_deposit_direct<float><<<blocks, 256, 0, st>>>(g, s, begin, n, fx, dc);
+    else k_deposit_direct<double><<<blocks, 256, 0, st>>>(g, s, begin, n, fx, dc);
     g_launches++;
 }
 
@@ -306,6 +323,7 @@ __device__ __forceinline__ long long fx_val(double t) {
     return __double_as_longlong(t) - __double_as_longlong(6755399441055744.0);
 }
 
+template <class R>
 __global__ void __launch_bounds__(kDepositThreads, 3)
     k_deposit_tiled(Geo g, PSet s, long long n, const Tile* __restrict__ tiles, const int* ntiles_p,
                     long long* __restrict__ fx, DevCounters* dc, int cap_nodes, double rho_cut) {
@@ -402,8 +420,8 @@ __global__ void __launch_bounds__(kDepositThreads, 3)
         unsigned long long fb = 0;
         long long clamps = 0;
         for (long long p = T.start + threadIdx.x; p < T.end; p += blockDim.x) {
-            const double psi = __ldcs(s.x[0] + p), theta = __ldcs(s.x[1] + p), zeta = __ldcs(s.x[2] + p),
-                         w = __ldcs(s.x[4] + p), mu = __ldcs(s.mu + p);
+            const double psi = ldp_cs<R>(s.x[0], p), theta = ldp_cs<R>(s.x[1], p), zeta = ldp_cs<R>(s.x[2], p),
+                         w = ldp_cs<R>(s.x[4], p), mu = ldp_cs<R>(s.mu, p);
             double r, invB, rho, inv_r;
             gyro_radius(g, psi, cos(theta), mu, &r, &invB, &rho, &inv_r);
             double wz1;
@@ -511,7 +529,10 @@ __global__ void __launch_bounds__(kDepositThreads, 3)
 }
 
 cudaError_t configure_deposit_tiled(size_t smem_bytes) {
-    return cudaFuncSetAttribute(k_deposit_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+    cudaError_t e = cudaFuncSetAttribute(k_deposit_tiled<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_bytes);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_deposit_tiled<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
 }
 
 void launch_deposit_tiled(const Geo& g, const PSet& s, long long n, const Tile* tiles, int max_tiles,
@@ -519,8 +540,12 @@ void launch_deposit_tiled(const Geo& g, const PSet& s, long long n, const Tile* 
                           cudaStream_t st) {
     (void)max_tiles;
     double rho_cut = deposit_rho_cut(g);
-    k_deposit_tiled<<<ctas, kDepositThreads, smem_bytes, st>>>(g, s, n, tiles, &dc->ntiles, fx, dc, cap_nodes,
-                                                              rho_cut);
+    if (g.prec32)
+        k_deposit_tiled<float><<<ctas, kDepositThreads, smem_bytes, st>>>(g, s, n, tiles, &dc->ntiles, fx, dc,
+                                                                          cap_nodes, rho_cut);
+    else
+        k_deposit_tiled<double><<<ctas, kDepositThreads, smem_bytes, st>>>(g, s, n, tiles, &dc->ntiles, fx, dc,
+                                                                           cap_nodes, rho_cut);
     g_launches++;
 }
 
@@ -733,7 +758,7 @@ __device__ __forceinline__ void push_epilogue(DevCounters* dc, double wmax, long
     if (nonfinite) dc->nonfinite = 1;
 }
 
-template <int MINB, bool CS, int GU = 8>
+template <int MINB, bool CS, int GU = 8, class R = double>
 __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long long n, double h,
                                              const double* __restrict__ gf, DevCounters* dc) {
     extern __shared__ RingTab rt_dyn[];
@@ -744,7 +769,7 @@ __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long lon
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
          p += (long long)gridDim.x * blockDim.x) {
         // CS: particle streams evict-first (.cs) so they do not push the field out of L2
-        auto ld = [&](const double* a) { return CS ? __ldcs(a + p) : a[p]; };
+        auto ld = [&](const double* a) { return CS ? ldp_cs<R>(a, p) : ldp<R>(a, p); };
         double base[5], X[5];
 #pragma unroll
         for (int d = 0; d < 5; d++) base[d] = ld(pp.base[d]);
@@ -753,10 +778,10 @@ __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long lon
         if (!(isfinite(X[0]) && isfinite(X[1]) && isfinite(X[2]) && isfinite(X[3]) && isfinite(X[4]))) nonfinite = 1;
 #pragma unroll
         for (int d = 0; d < 5; d++) {
-            if (CS) __stcs(pp.out[d] + p, X[d]);
-            else pp.out[d][p] = X[d];
+            if (CS) stp_cs<R>(pp.out[d], p, X[d]);
+            else stp<R>(pp.out[d], p, X[d]);
         }
-        wmax = fmax(wmax, fabs(X[4]));
+        wmax = fmax(wmax, fabs((double)(R)X[4]));
     }
     push_epilogue(dc, wmax, refl, clamps, nonfinite);
 }
@@ -1062,7 +1087,11 @@ void launch_push3(const Geo& g, const double* const src[5], const double* const 
         return e ? atoi(e) : 4;
     }();
     const bool stage2 = (base[0] != src[0]);
-    if (variant == 0) {
+    if (g.prec32) {  // fp32 state: the plain fused kernel
+        int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
+        size_t smr = (g.mpsi + 1) * sizeof(RingTab);
+        k_push<2, true, 8, float><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
+    } else if (variant == 0) {
         // TMA-staged persistent kernel, 2 CTAs per SM
         int nsm = 148;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
@@ -1094,18 +1123,20 @@ void launch_push3(const Geo& g, const double* const src[5], const double* const 
     g_launches++;
 }
 
+template <class R>
 __global__ void k_wmax(const double* __restrict__ w, long long n, DevCounters* dc) {
     double m = 0.0;
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
          p += (long long)gridDim.x * blockDim.x)
-        m = fmax(m, fabs(w[p]));
+        m = fmax(m, fabs(ldp<R>(w, p)));
     m = warp_max(m);
     if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(&dc->wmax_bits, (unsigned long long)__double_as_longlong(m));
 }
 
 void launch_wmax(const double* w, long long n, DevCounters* dc, cudaStream_t st) {
     int blocks = (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148LL * 8));
-    k_wmax<<<blocks, 256, 0, st>>>(w, n, dc);
+    if (g_prec32) k_wmax<float><<<blocks, 256, 0, st>>>(w, n, dc);
+    else k_wmax<double><<<blocks, 256, 0, st>>>(w, n, dc);
     g_launches++;
 }
 
@@ -1130,6 +1161,7 @@ __device__ __forceinline__ unsigned bin_key(const Geo& g, double psi, double the
     return (unsigned)((__ldg(g.igrid + i) + c) * g.P + k);
 }
 
+template <class R>
 __global__ void k_bin_keys(Geo g, PSet s, long long n, unsigned* __restrict__ key, unsigned* __restrict__ rank,
                            unsigned* __restrict__ count) {
     // cell-sorted input repeats a key ~100 times in a row: aggregate equal keys
@@ -1138,7 +1170,7 @@ __global__ void k_bin_keys(Geo g, PSet s, long long n, unsigned* __restrict__ ke
     for (long long p0 = (long long)blockIdx.x * blockDim.x; p0 < n; p0 += (long long)gridDim.x * blockDim.x) {
         const long long p = p0 + threadIdx.x;
         const bool act = p < n;
-        unsigned kk = act ? bin_key(g, s.x[0][p], s.x[1][p], s.x[2][p]) : 0xffffffffu;
+        unsigned kk = act ? bin_key(g, ldp<R>(s.x[0], p), ldp<R>(s.x[1], p), ldp<R>(s.x[2], p)) : 0xffffffffu;
         const unsigned peers = __match_any_sync(0xffffffffu, kk);
         const int leader = __ffs(peers) - 1;
         unsigned base = 0;
@@ -1155,7 +1187,8 @@ void launch_bin_keys(const Geo& g, const PSet& s, long long n, unsigned* key, un
                      cudaStream_t st) {
     if (n <= 0) return;
     int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
-    k_bin_keys<<<blocks, 256, 0, st>>>(g, s, n, key, rank, count);
+    if (g.prec32) k_bin_keys<float><<<blocks, 256, 0, st>>>(g, s, n, key, rank, count);
+    else k_bin_keys<double><<<blocks, 256, 0, st>>>(g, s, n, key, rank, count);
     g_launches++;
 }
 
@@ -1290,35 +1323,37 @@ struct PermArrays {
     unsigned long long* id_dst;
 };
 
+template <class R>
 __global__ void k_gather_perm_multi(PermArrays A, const unsigned* __restrict__ inv, long long n) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const long long s = inv[i];
-        double v[12];
+        R v[12];
 #pragma unroll
         for (int a = 0; a < 12; a++)
-            if (a < A.na) v[a] = __ldg(A.src[a] + s);
+            if (a < A.na) v[a] = __ldg(reinterpret_cast<const R*>(A.src[a]) + s);
         unsigned long long id = A.id_src ? __ldg(A.id_src + s) : 0ull;
 #pragma unroll
         for (int a = 0; a < 12; a++)
-            if (a < A.na) __stcs(A.dst[a] + i, v[a]);
+            if (a < A.na) __stcs(reinterpret_cast<R*>(A.dst[a]) + i, v[a]);
         if (A.id_src) A.id_dst[i] = id;
     }
 }
 
 // scatter form: dst_a[dest[p]] = src_a[p] (coalesced reads; on nearly sorted
 // input the writes come in runs)
+template <class R>
 __global__ void k_scatter_perm_multi(PermArrays A, const unsigned* __restrict__ dest, long long n) {
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
          p += (long long)gridDim.x * blockDim.x) {
         const long long d = dest[p];
-        double v[12];
+        R v[12];
 #pragma unroll
         for (int a = 0; a < 12; a++)
-            if (a < A.na) v[a] = __ldcs(A.src[a] + p);
+            if (a < A.na) v[a] = __ldcs(reinterpret_cast<const R*>(A.src[a]) + p);
 #pragma unroll
         for (int a = 0; a < 12; a++)
-            if (a < A.na) A.dst[a][d] = v[a];
+            if (a < A.na) reinterpret_cast<R*>(A.dst[a])[d] = v[a];
         if (A.id_src) A.id_dst[d] = A.id_src[p];
     }
 }
@@ -1335,7 +1370,8 @@ void launch_scatter_perm_multi(const double* const* src, double* const* dst, int
     A.id_src = id_src;
     A.id_dst = id_dst;
     int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
-    k_scatter_perm_multi<<<blocks, 256, 0, st>>>(A, dest, n);
+    if (g_prec32) k_scatter_perm_multi<float><<<blocks, 256, 0, st>>>(A, dest, n);
+    else k_scatter_perm_multi<double><<<blocks, 256, 0, st>>>(A, dest, n);
     g_launches++;
 }
 
@@ -1351,14 +1387,18 @@ void launch_gather_perm_multi(const double* const* src, double* const* dst, int 
     A.id_src = id_src;
     A.id_dst = id_dst;
     int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
-    k_gather_perm_multi<<<blocks, 256, 0, st>>>(A, inv, n);
+    if (g_prec32) k_gather_perm_multi<float><<<blocks, 256, 0, st>>>(A, inv, n);
+    else k_gather_perm_multi<double><<<blocks, 256, 0, st>>>(A, inv, n);
     g_launches++;
 }
 
 void launch_gather_perm_f64(const double* src, double* dst, const unsigned* inv, long long n, cudaStream_t st) {
     if (n <= 0) return;
     int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
-    k_gather_perm<double><<<blocks, 256, 0, st>>>(src, dst, inv, n);
+    if (g_prec32)
+        k_gather_perm<float><<<blocks, 256, 0, st>>>(reinterpret_cast<const float*>(src), reinterpret_cast<float*>(dst),
+                                                     inv, n);
+    else k_gather_perm<double><<<blocks, 256, 0, st>>>(src, dst, inv, n);
     g_launches++;
 }
 
@@ -1484,10 +1524,11 @@ void launch_build_tiles(const Geo& g, const unsigned* offset, int tile_max, Tile
 }
 
 // deterministic sum: fixed grid of partials, then one block in fixed order
+template <class R>
 __global__ void k_sum_partial(const double* __restrict__ x, long long n, double* __restrict__ partial) {
     double s = 0.0;
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x)
-        s += x[p];
+        s += ldp<R>(x, p);
     __shared__ double sm[32];
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
@@ -1509,7 +1550,8 @@ __global__ void k_sum_final(const double* __restrict__ partial, int nb, double* 
 
 void launch_sum_f64(const double* x, long long n, double* out, double* partial, cudaStream_t st) {
     const int nb = 592;
-    k_sum_partial<<<nb, 256, 0, st>>>(x, n, partial);
+    if (g_prec32) k_sum_partial<float><<<nb, 256, 0, st>>>(x, n, partial);
+    else k_sum_partial<double><<<nb, 256, 0, st>>>(x, n, partial);
     k_sum_final<<<1, 32, 0, st>>>(partial, nb, out);
     g_launches += 2;
 }
@@ -1521,27 +1563,31 @@ void launch_sum_i64_pair(const long long* in2, long long* out, cudaStream_t st) 
     g_launches++;
 }
 
+template <class R>
 __global__ void k_fill_f64(double* __restrict__ x, long long n, double v) {
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x)
-        x[p] = v;
+        stp<R>(x, p, v);
 }
 
 void launch_fill_f64(double* x, long long n, double v, cudaStream_t st) {
     if (n <= 0) return;
     int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
-    k_fill_f64<<<blocks, 256, 0, st>>>(x, n, v);
+    if (g_prec32) k_fill_f64<float><<<blocks, 256, 0, st>>>(x, n, v);
+    else k_fill_f64<double><<<blocks, 256, 0, st>>>(x, n, v);
     g_launches++;
 }
 
+template <class R>
 __global__ void k_gather_f64(const double* __restrict__ src, const long long* __restrict__ idx, long long m,
                              double* __restrict__ out) {
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < m; q += (long long)gridDim.x * blockDim.x)
-        out[q] = src[idx[q]];
+        out[q] = ldp<R>(src, idx[q]);
 }
 
 void launch_gather_f64(const double* src, const long long* idx, long long m, double* out, cudaStream_t st) {
     int blocks = (int)std::max<long long>(1, std::min<long long>((m + 255) / 256, 148LL * 8));
-    k_gather_f64<<<blocks, 256, 0, st>>>(src, idx, m, out);
+    if (g_prec32) k_gather_f64<float><<<blocks, 256, 0, st>>>(src, idx, m, out);
+    else k_gather_f64<double><<<blocks, 256, 0, st>>>(src, idx, m, out);
     g_launches++;
 }
 
@@ -1575,6 +1621,7 @@ struct Philox {
     }
 };
 
+template <class R>
 __global__ void k_load(Geo g, PSet s, long long n, unsigned long long seed, long long id0, double w_amp,
                        double vcut, double zlo, double zhi, double rlo, double rhi) {
     const double jmax = (1.0 + g.a1 * g.inv_R0) * (1.0 + g.a1 * g.inv_R0);
@@ -1608,12 +1655,12 @@ __global__ void k_load(Geo g, PSet s, long long n, unsigned long long seed, long
             vperp = sqrt(-2.0 * log(1.0 - rng.u53()));
         } while (vperp > vcut);
         double B = 1.0 / (1.0 + r * g.inv_R0 * cos(th));
-        s.x[0][p] = 0.5 * r * r;
-        s.x[1][p] = th;
-        s.x[2][p] = ze;
-        s.x[3][p] = vpar / (g.omega0 * B);
-        s.x[4][p] = w_amp * (2.0 * rng.u53() - 1.0);
-        s.mu[p] = vperp * vperp / (2.0 * B);
+        stp<R>(s.x[0], p, 0.5 * r * r);
+        stp<R>(s.x[1], p, th);
+        stp<R>(s.x[2], p, ze);
+        stp<R>(s.x[3], p, vpar / (g.omega0 * B));
+        stp<R>(s.x[4], p, w_amp * (2.0 * rng.u53() - 1.0));
+        stp<R>(s.mu, p, vperp * vperp / (2.0 * B));
         if (s.id) s.id[p] = gid;
     }
 }
@@ -1622,7 +1669,8 @@ void launch_load(const Geo& g, const PSet& s, long long n, unsigned long long se
                  double vcut, double zlo, double zhi, double rlo, double rhi, cudaStream_t st) {
     if (n <= 0) return;
     int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
-    k_load<<<blocks, 256, 0, st>>>(g, s, n, seed, id0, w_amp, vcut, zlo, zhi, rlo, rhi);
+    if (g.prec32) k_load<float><<<blocks, 256, 0, st>>>(g, s, n, seed, id0, w_amp, vcut, zlo, zhi, rlo, rhi);
+    else k_load<double><<<blocks, 256, 0, st>>>(g, s, n, seed, id0, w_amp, vcut, zlo, zhi, rlo, rhi);
     g_launches++;
 }
 

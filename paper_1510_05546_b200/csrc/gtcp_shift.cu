@@ -70,6 +70,7 @@ __device__ __forceinline__ int radial_domain(const Geo& g, double psi) {
 // classify: cls[p] in {0 keep, 1 left, 2 right}; per-chunk mover counts.
 // mode 0: toroidal (periodic ring, the shorter way round); mode 1: radial
 // (inner = left, outer = right, not periodic)
+template <class R>
 __global__ void __launch_bounds__(kShiftBlock) k_shift_classify(Geo g, const double* __restrict__ zeta,
                                                                 const double* __restrict__ psi, int mode, long long n,
                                                                 unsigned char* __restrict__ cls,
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(kShiftBlock) k_shift_classify(Geo g, const dou
 #pragma unroll
     for (int it = 0; it < kIt; it++) {
         long long p = warp_p(base, it);
-        z[it] = (p < n) ? __ldcs(key + p) : 0.0;
+        z[it] = (p < n) ? (double)__ldcs(reinterpret_cast<const R*>(key) + p) : 0.0;
     }
     unsigned a = 0, b = 0;
 #pragma unroll
@@ -182,6 +183,7 @@ __global__ void __launch_bounds__(kShiftBlock) k_shift_pack(const unsigned char*
 
 // dst.a[d][q] = src.a[d][idx[q]] (gather; dst contiguous) or, with scatter,
 // dst.a[d][didx[q]] = src.a[d][idx[q]]; one thread per (q, d), d = blockIdx.y
+template <class R>
 __global__ void k_shift_copy(ShiftAttrs src, ShiftAttrs dst, const unsigned* __restrict__ idx,
                              const unsigned* __restrict__ didx, long long m, const unsigned* __restrict__ m_dev) {
     const int d = blockIdx.y;
@@ -190,13 +192,13 @@ __global__ void k_shift_copy(ShiftAttrs src, ShiftAttrs dst, const unsigned* __r
         const long long s = idx[q];
         const long long o = didx ? (long long)didx[q] : q;
         if (d < src.nattr) {
-            double v = 0.0;
+            R v = 0;
 #pragma unroll
             for (int e = 0; e < 11; e++)
-                if (e == d) v = src.a[e][s];
+                if (e == d) v = reinterpret_cast<const R*>(src.a[e])[s];
 #pragma unroll
             for (int e = 0; e < 11; e++)
-                if (e == d) dst.a[e][o] = v;
+                if (e == d) reinterpret_cast<R*>(dst.a[e])[o] = v;
         } else if (src.id) {
             dst.id[o] = src.id[s];
         }
@@ -277,7 +279,8 @@ int shift_chunks(long long n) { return (int)std::max<long long>(1, (n + kChunk -
 void launch_shift_classify(const Geo& g, const double* zeta, const double* psi, int mode, long long n,
                            unsigned char* cls, unsigned* cntL, unsigned* cntR, cudaStream_t st) {
     int nb = shift_chunks(n);
-    k_shift_classify<<<nb, kShiftBlock, 0, st>>>(g, zeta, psi, mode, n, cls, cntL, cntR);
+    if (g.prec32) k_shift_classify<float><<<nb, kShiftBlock, 0, st>>>(g, zeta, psi, mode, n, cls, cntL, cntR);
+    else k_shift_classify<double><<<nb, kShiftBlock, 0, st>>>(g, zeta, psi, mode, n, cls, cntL, cntR);
     g_launches++;
 }
 
@@ -317,8 +320,12 @@ void launch_shift_pack(double* const* attrs, int nattr, unsigned long long* id, 
         if (m == 0) continue;
         int gx = (int)std::min<long long>((m + 255) / 256, 148LL * 8);
         dim3 grid(gx, nattr + (id ? 1 : 0));
-        k_shift_copy<<<grid, 256, 0, st>>>(A, side ? mk(sendR, nattr, idR) : mk(sendL, nattr, idL), side ? idxR : idxL,
-                                           nullptr, m, nullptr);
+        if (g_prec32)
+            k_shift_copy<float><<<grid, 256, 0, st>>>(A, side ? mk(sendR, nattr, idR) : mk(sendL, nattr, idL),
+                                                      side ? idxR : idxL, nullptr, m, nullptr);
+        else
+            k_shift_copy<double><<<grid, 256, 0, st>>>(A, side ? mk(sendR, nattr, idR) : mk(sendL, nattr, idL),
+                                                       side ? idxR : idxL, nullptr, m, nullptr);
         g_launches++;
     }
 }
@@ -335,7 +342,8 @@ void launch_shift_backfill(double* const* attrs, int nattr, unsigned long long* 
         ShiftAttrs A = mk(attrs, nattr, id);
         int gx = (int)std::min<long long>((nholes + 255) / 256, 148LL * 8);
         dim3 grid(gx, nattr + (id ? 1 : 0));
-        k_shift_copy<<<grid, 256, 0, st>>>(A, A, fills, holes, nholes, nholes_dev);
+        if (g_prec32) k_shift_copy<float><<<grid, 256, 0, st>>>(A, A, fills, holes, nholes, nholes_dev);
+        else k_shift_copy<double><<<grid, 256, 0, st>>>(A, A, fills, holes, nholes, nholes_dev);
         g_launches++;
     }
 }

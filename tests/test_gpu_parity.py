@@ -315,3 +315,64 @@ def test_toroidal_decomposition_parity_2gpu(G, args):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert '"ok": true' in r.stdout
+
+
+# ------------------------------------------------------------------ fp32 state (class D precision)
+TOL32 = 1e-4
+
+
+def _round32(parts):
+    out = dict(parts)
+    for k in ("psi", "theta", "zeta", "rho", "w", "mu"):
+        out[k] = parts[k].astype(np.float32).astype(np.float64)
+    # keep angles inside [0, 2 pi) after rounding
+    for k in ("theta", "zeta"):
+        out[k] = np.where(out[k] >= TWO_PI, 0.0, out[k])
+    return out
+
+
+def test_fp32_charge_and_step_parity(G, orc, T):
+    """precision = 32: fp32 particle state, fp64 arithmetic.  Charge grid and
+    one full step against the oracle fed the same fp32-rounded state."""
+    cfg, p, g, parts = T
+    parts32 = _round32(parts)
+    ctx = G.Context(G.gtcp_default_params("T", track_ids=1, precision=32))
+    ctx.set_particles(parts32)
+    ctx.charge()
+    got = ctx.get_grid(G.GRID_CHARGE)
+    ref = orc.charge_global(p, parts32)
+    assert rel_err(got, ref) <= TOL32
+    nm = orc.marker_norm(p, parts32)
+    ctx2 = G.Context(G.gtcp_default_params("T", track_ids=1, precision=32))
+    ctx2.set_particles(parts32)
+    ctx2.set_grid(G.GRID_MARKER, nm)
+    ctx2.step(1)
+    gotp = ctx2.get_particles()
+    ref_state = {k: v.copy() for k, v in parts32.items()}
+    orc.step_global(p, ref_state, nm)
+    o1, o2 = np.argsort(gotp["id"]), np.argsort(ref_state["id"])
+    assert np.array_equal(gotp["id"][o1], ref_state["id"][o2])
+    for k in ("psi", "rho", "w"):
+        assert rel_err(gotp[k][o1], ref_state[k][o2]) <= TOL32, k
+    for k in ("theta", "zeta"):
+        assert float(np.max(np.abs(circ(gotp[k][o1], ref_state[k][o2])))) / TWO_PI <= TOL32, k
+
+
+def test_fp32_full_A_load_charge_conservation(G, orc):
+    """fp32 store at full class A size: load, charge conservation, tiled == direct."""
+    ctx = G.Context(G.gtcp_default_params("A", precision=32))
+    ctx.load()
+    ctx.charge()
+    a = ctx.get_grid(G.GRID_CHARGE)
+    st = ctx.stats()
+    cfg = synth.config("A")
+    g = orc.geometry(orc.make_params(cfg))
+    canon = sum(a[:64, g.igrid[i]:g.igrid[i] + g.mtheta[i]].sum() for i in range(cfg["mpsi"] + 1))
+    n = ctx.get_info().n_local
+    assert abs(canon - st["sum_w"]) <= 1e-9 * n * cfg["w_init_amp"] / 2
+    ctx.set_charge_mode(1)
+    ctx.charge()
+    assert np.array_equal(a, ctx.get_grid(G.GRID_CHARGE))
+    ctx.step(2)
+    assert ctx.stats()["n_global"] == n
+    ctx.close()
