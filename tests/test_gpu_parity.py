@@ -376,3 +376,31 @@ def test_fp32_full_A_load_charge_conservation(G, orc):
     ctx.step(2)
     assert ctx.stats()["n_global"] == n
     ctx.close()
+
+
+def test_fp32_D_geometry_charge_and_push(G, orc):
+    """Class D geometry (mpsi=768, mthetamax=5632: 2,406,883 nodes per plane),
+    fp32 state, 4 planes to keep the oracle fast: charge and a stage-1 push
+    against the oracle on the same fp32-rounded markers."""
+    over = dict(mzetamax=4)
+    cfg = synth.config("D", **over)
+    p = orc.make_params(cfg)
+    g = orc.geometry(p)
+    assert g.mgrid == 2406883
+    parts = _round32(synth.load_particles(cfg, 200_000, seed=4, w_amp=0.1))
+    ctx = G.Context(G.gtcp_default_params("D", track_ids=1, precision=32, **over))
+    ctx.set_particles(parts)
+    ctx.charge()
+    assert rel_err(ctx.get_grid(G.GRID_CHARGE), orc.charge_global(p, parts)) <= TOL32
+    gp = _smooth_field(orc, p, g)
+    ctx.set_grid(G.GRID_GRADPHI, gp)
+    Xa = {k: parts[k].copy() for k in orc.ATTRS}
+    Xb = {k: parts[k].copy() for k in orc.ATTRS}
+    ctx.push(1)
+    orc.push(p, 1, Xa, Xb, parts["mu"], gp)
+    got = ctx.get_particles()
+    o1, o2 = np.argsort(got["id"]), np.argsort(parts["id"])
+    for k in ("psi", "rho", "w"):
+        assert rel_err(got[k][o1], Xb[k][o2]) <= TOL32, k
+    for k in ("theta", "zeta"):
+        assert float(np.max(np.abs(circ(got[k][o1], Xb[k][o2])))) / TWO_PI <= TOL32, k

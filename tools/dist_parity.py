@@ -29,6 +29,7 @@ ap.add_argument("--w-amp", type=float, default=None)
 ap.add_argument("--mzetamax", type=int, default=None)
 ap.add_argument("--npartdom", type=int, default=1)
 ap.add_argument("--nradial", type=int, default=1)
+ap.add_argument("--precision", type=int, default=64)
 a = ap.parse_args()
 
 rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
@@ -41,10 +42,17 @@ cfg = synth.config(a.size, **over)
 npd, nrad = a.npartdom, a.nradial
 ntor = world // (npd * nrad)
 rank_t, rank_r, rank_p = rank // (npd * nrad), (rank // npd) % nrad, rank % npd
-params = G.gtcp_default_params(a.size, ntoroidal=ntor, npartdom=npd, nradial=nrad, track_ids=1, bin_every=1, **over)
+params = G.gtcp_default_params(a.size, ntoroidal=ntor, npartdom=npd, nradial=nrad, track_ids=1, bin_every=1,
+                                precision=a.precision, **over)
 geo = G.gtcp_geometry(params)
 n = a.nparts or cfg["micell"] * (geo["mgrid"] - cfg["mpsi"]) * cfg["mzetamax"]
 parts = synth.load_particles(cfg, n, seed=1, w_amp=a.w_amp)
+TOLP = 1e-6 if a.precision == 64 else 1e-4
+if a.precision == 32:  # the oracle sees the same fp32-rounded state
+    for _k in ("psi", "theta", "zeta", "rho", "w", "mu"):
+        parts[_k] = parts[_k].astype(np.float32).astype(np.float64)
+    for _k in ("theta", "zeta"):
+        parts[_k] = np.where(parts[_k] >= 2 * math.pi, 0.0, parts[_k])
 P = cfg["mzetamax"] // ntor
 # G-6 radial windows: equal-area split snapped to the nearest ring (test-side restatement)
 _dr = (cfg["a1"] - cfg["a0"]) / cfg["mpsi"]
@@ -131,13 +139,19 @@ for step in range(a.steps):
         err["charge"] = ce / float(np.max(np.abs(ch_ref)))
         err["movers_sent"] = int(st["movers_sent"])
         report[f"step{step}"] = err
-        ok &= err["count"] == 1 and err["owner"] == 1 and all(err[k] <= 1e-6 for k in ("psi", "rho", "w", "theta", "zeta", "charge"))
+        ok &= err["count"] == 1 and err["owner"] == 1 and all(err[k] <= TOLP for k in ("psi", "rho", "w", "theta", "zeta", "charge"))
         # continue both sides from the oracle state (identical inputs each step)
     # reset every rank to the oracle trajectory for the next step
     obj = [orc_state if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     st_all = obj[0]
     if rank != 0:
+        orc_state = st_all
+    if a.precision == 32:  # the library stores fp32: restart both sides from the rounded state
+        for _k in ("psi", "theta", "zeta", "rho", "w", "mu"):
+            st_all[_k] = st_all[_k].astype(np.float32).astype(np.float64)
+        for _k in ("theta", "zeta"):
+            st_all[_k] = np.where(st_all[_k] >= 2 * math.pi, 0.0, st_all[_k])
         orc_state = st_all
     zz = np.minimum(np.floor(st_all["zeta"] * cz).astype(np.int64), cfg["mzetamax"] - 1)
     sel = ((zz // P) == rank_t) & (rdom(st_all["psi"]) == rank_r) & ((st_all["id"] % npd) == rank_p)
