@@ -43,6 +43,17 @@ __device__ __forceinline__ double plane_interp(const Geo& g, const double* pl, d
     return (1.0 - wp1) * ring_interp(g, pl, i, th, zk) + wp1 * ring_interp(g, pl, i + 1, th, zk);
 }
 
+// F-1 four-point gyro-average at node (ring i, label j) of plane array pl.
+// The two theta-points sit on ring i itself (r = r_i: the radial weight of
+// ring i is 1 up to rounding), so they interpolate on ring i only.
+__device__ __forceinline__ double gyro_value(const Geo& g, const double* pl, int i, int j, int mt, double zk) {
+    const double r = g.a0 + i * g.dr;
+    const double th = j * (GTCP_TWO_PI / mt) + zk * __ldg(g.qtinv + i);
+    const double dth = g.rhoG / r;
+    return 0.25 * (plane_interp(g, pl, r + g.rhoG, th, zk) + ring_interp(g, pl, i, th + dth, zk) +
+                   plane_interp(g, pl, r - g.rhoG, th, zk) + ring_interp(g, pl, i, th - dth, zk));
+}
+
 // copy canonical j=0 into the duplicate j=mtheta on `planes` planes (ncomp interleaved)
 __global__ void k_fill_dup(Geo g, double* f, int planes, int ncomp) {
     long long total = (long long)planes * (g.mpsi + 1) * ncomp;
@@ -250,12 +261,7 @@ __global__ void k_gyro(Geo g, const double* __restrict__ in, double* __restrict_
         int j = node - __ldg(g.igrid + i);
         if (j == mt) j = 0;
         const double* pl = in + (long long)k * g.mgrid;
-        double zk = (double)(g.k0 + k) * g.dzeta;
-        double r = g.a0 + i * g.dr;
-        double th = j * (GTCP_TWO_PI / mt) + zk * __ldg(g.qtinv + i);
-        double v = plane_interp(g, pl, r + g.rhoG, th, zk) + plane_interp(g, pl, r, th + g.rhoG / r, zk) +
-                   plane_interp(g, pl, r - g.rhoG, th, zk) + plane_interp(g, pl, r, th - g.rhoG / r, zk);
-        out[e] = 0.25 * v;
+        out[e] = gyro_value(g, pl, i, j, mt, (double)(g.k0 + k) * g.dzeta);
     }
 }
 
@@ -290,12 +296,8 @@ __global__ void k_gyro_jacobi(Geo g, const double* __restrict__ g1, const double
         int j = node - __ldg(g.igrid + i);
         if (j == mt) j = 0;
         const double* pl = g1 + (long long)k * g.mgrid;
-        double zk = (double)(g.k0 + k) * g.dzeta;
-        double r = g.a0 + i * g.dr;
-        double th = j * (GTCP_TWO_PI / mt) + zk * __ldg(g.qtinv + i);
-        double v = plane_interp(g, pl, r + g.rhoG, th, zk) + plane_interp(g, pl, r, th + g.rhoG / r, zk) +
-                   plane_interp(g, pl, r - g.rhoG, th, zk) + plane_interp(g, pl, r, th - g.rhoG / r, zk);
-        phi[e] = (1.0 - omega) * phi[e] + omega * (rhs[e] + 0.25 * v) / c0;
+        const double v = gyro_value(g, pl, i, j, mt, (double)(g.k0 + k) * g.dzeta);
+        phi[e] = (1.0 - omega) * phi[e] + omega * (rhs[e] + v) / c0;
     }
 }
 
