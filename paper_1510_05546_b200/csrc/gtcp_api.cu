@@ -84,6 +84,7 @@ struct gtcp_ctx_s {
     long long* d_counts = nullptr;  // [myL, myR, fromRight, fromLeft, mine, total]
     long long* h_counts = nullptr;  // pinned mirror
     int shift_blocks = 0;
+    bool cls_ready = false;  // cls + per-chunk counts of the toroidal shift were produced by the push
     long long movers_sent = 0, movers_recv = 0;
     // charge config
     int charge_mode = 0;
@@ -747,6 +748,8 @@ extern "C" gtcp_status gtcp_field(gtcp_ctx c) {
 // ----------------------------------------------------------------------------
 // push
 // ----------------------------------------------------------------------------
+#define CU_VOID(call) do { (void)(call); } while (0)
+
 // push over [0, n): the binned part tile by tile (field windows staged in
 // shared memory), the tail (shift arrivals beyond the last bin) plainly
 static void push_range(gtcp_ctx c, double* const* src, double* const* base, double* const* out, double h) {
@@ -761,6 +764,12 @@ static void push_range(gtcp_ctx c, double* const* src, double* const* base, doub
         tiled_end = std::min(c->n, c->n_binned);
         launch_push_tiled(c->geo, src, base, out, c->mu, tiled_end, h, c->gfield, c->tiles, c->dc, c->st);
     }
+    // fused toroidal classification for the shift that follows (plain kernel only)
+    const bool fuse = c->prm.ntoroidal > 1 && tiled_end == 0 && c->cls != nullptr;
+    unsigned* cntL = c->bcount;
+    unsigned* cntR = cntL + (c->shift_blocks + 1);
+    if (fuse) CU_VOID(cudaMemsetAsync(cntL, 0, 2 * (c->shift_blocks + 1) * sizeof(unsigned), c->st));
+    c->cls_ready = fuse;
     if (c->n > tiled_end) {
         const double* s2[5];
         const double* b2[5];
@@ -770,7 +779,8 @@ static void push_range(gtcp_ctx c, double* const* src, double* const* base, doub
             b2[d] = pofs(base[d], tiled_end);
             o2[d] = pofs(out[d], tiled_end);
         }
-        launch_push3(c->geo, s2, b2, o2, pofs(c->mu, tiled_end), c->n - tiled_end, h, c->gfield, c->dc, c->st);
+        launch_push3(c->geo, s2, b2, o2, pofs(c->mu, tiled_end), c->n - tiled_end, h, c->gfield, c->dc, c->st,
+                     fuse ? c->cls : nullptr, fuse ? cntL : nullptr, fuse ? cntR : nullptr);
     }
 }
 
@@ -805,6 +815,7 @@ extern "C" gtcp_status gtcp_push(gtcp_ctx c, int stage) {
 // ----------------------------------------------------------------------------
 static gtcp_status do_bin(gtcp_ctx c) {
     const Geo& g = c->geo;
+    c->cls_ready = false;
     PSet s = live_set(c);
     CU(cudaMemsetAsync(c->count, 0, (c->nkeys + 1) * sizeof(unsigned), c->st));
     launch_bin_keys(g, s, c->n, c->key, c->rankbuf, c->count, c->st);
@@ -1223,7 +1234,12 @@ gtcp_status shift_exchange(gtcp_ctx c, int dir) {
         unsigned* offR = offL + (c->shift_blocks + 1);
         unsigned* offH = offR + (c->shift_blocks + 1);
         unsigned* offF = offH + (c->shift_blocks + 1);
-        launch_shift_classify(g, attrs[2], attrs[0], dir, n, c->cls, cntL, cntR, c->st);
+        if (dir == 0 && iter == 0 && c->cls_ready) {
+            // classification and per-chunk counts came fused out of the push
+        } else {
+            launch_shift_classify(g, attrs[2], attrs[0], dir, n, c->cls, cntL, cntR, c->st);
+        }
+        if (dir == 0) c->cls_ready = false;
         launch_scan_u32(cntL, offL, nb, c->scan_tmp, c->st);
         launch_scan_u32(cntR, offR, nb, c->scan_tmp, c->st);
         launch_shift_nkeep(n, offL + nb, offR + nb, c->d_nkeep, c->d_counts, c->st);

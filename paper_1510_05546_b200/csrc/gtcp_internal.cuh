@@ -76,7 +76,8 @@ void launch_fx_scale(DevCounters* dc, cudaStream_t st);
 void launch_fx_to_real(const Geo& g, const long long* fx, double* rho, const DevCounters* dc, int planes,
                        cudaStream_t st);
 void launch_push3(const Geo& g, const double* const src[5], const double* const base[5], double* const out[5],
-                  const double* mu, long long n, double h, const double* gfield, DevCounters* dc, cudaStream_t st);
+                  const double* mu, long long n, double h, const double* gfield, DevCounters* dc, cudaStream_t st,
+                  unsigned char* cls = nullptr, unsigned* cntL = nullptr, unsigned* cntR = nullptr);
 void launch_push_tiled(const Geo& g, const double* const src[5], const double* const base[5], double* const out[5],
                        const double* mu, long long n, double h, const double* gfield, const Tile* tiles,
                        DevCounters* dc, cudaStream_t st);

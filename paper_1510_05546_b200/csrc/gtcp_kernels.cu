@@ -596,7 +596,25 @@ struct PushPtrs {
     const double* base[5];
     double* out[5];
     const double* mu;
+    // optional fused toroidal shift classification (H-1) of the new state:
+    // cls[p] in {0 keep, 1 left, 2 right}, per-16384-particle-chunk mover counts
+    unsigned char* cls;
+    unsigned* cntL;
+    unsigned* cntR;
 };
+
+static constexpr int kShiftChunkLog2 = 14;  // == log2(kChunk) of gtcp_shift.cu
+
+// same expression as the shift's classify (mode 0): destination toroidal domain
+// floor(kg / P) of the new zeta, the shorter way round the torus
+__device__ __forceinline__ unsigned char toroidal_class(const Geo& g, double zeta) {
+    double wz1;
+    const int d = plane_of(g, zeta, &wz1) / g.P;
+    int rel = d - g.rank_t;
+    if (rel < 0) rel += g.ntor;
+    if (rel == 0) return 0;
+    return (rel <= g.ntor / 2) ? 2 : 1;
+}
 
 __device__ __forceinline__ double warp_max(double v) {
     for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -780,6 +798,18 @@ __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long lon
         for (int d = 0; d < 5; d++) {
             if (CS) stp_cs<R>(pp.out[d], p, X[d]);
             else stp<R>(pp.out[d], p, X[d]);
+        }
+        if (pp.cls) {
+            // classify on the value as stored (fp32 state rounds zeta)
+            const unsigned char c = toroidal_class(g, (double)(R)X[2]);
+            pp.cls[p] = c;
+            // the 32 lanes of a warp hold consecutive p inside one chunk
+            const unsigned act = __activemask();
+            const unsigned bl = __ballot_sync(act, c == 1), br = __ballot_sync(act, c == 2);
+            if ((threadIdx.x & 31) == __ffs(act) - 1) {
+                if (bl) atomicAdd(pp.cntL + (p >> kShiftChunkLog2), (unsigned)__popc(bl));
+                if (br) atomicAdd(pp.cntR + (p >> kShiftChunkLog2), (unsigned)__popc(br));
+            }
         }
         wmax = fmax(wmax, fabs((double)(R)X[4]));
     }
@@ -1057,6 +1087,8 @@ void launch_push_tiled(const Geo& g, const double* const src[5], const double* c
         pp.out[d] = out[d];
     }
     pp.mu = mu;
+    pp.cls = nullptr;
+    pp.cntL = pp.cntR = nullptr;
     const int win_cap = 1024;  // nodes of 48 B: 48 KB of windows per CTA
     size_t sm = push_tiled_smem(g, win_cap);
     static bool cfg = (cudaFuncSetAttribute(k_push_tiled<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1073,7 +1105,7 @@ void launch_push_tiled(const Geo& g, const double* const src[5], const double* c
 
 void launch_push3(const Geo& g, const double* const src[5], const double* const base[5], double* const out[5],
                   const double* mu, long long n, double h, const double* gfield, DevCounters* dc,
-                  cudaStream_t st) {
+                  cudaStream_t st, unsigned char* cls, unsigned* cntL, unsigned* cntR) {
     if (n <= 0) return;
     PushPtrs pp;
     for (int d = 0; d < 5; d++) {
@@ -1082,11 +1114,16 @@ void launch_push3(const Geo& g, const double* const src[5], const double* const 
         pp.out[d] = out[d];
     }
     pp.mu = mu;
-    static int variant = [] {
+    pp.cls = cls;
+    pp.cntL = cntL;
+    pp.cntR = cntR;
+    static const int variant0 = [] {
         const char* e = getenv("GTCP_PUSH_VARIANT");
         return e ? atoi(e) : 4;
     }();
+    int variant = variant0;
     const bool stage2 = (base[0] != src[0]);
+    if (cls) variant = 4;  // fused classification lives in the plain kernel
     if (g.prec32) {  // fp32 state: the plain fused kernel
         int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
         size_t smr = (g.mpsi + 1) * sizeof(RingTab);
@@ -1493,28 +1530,100 @@ __device__ __forceinline__ int ring_tiles(const Geo& g, int i, const unsigned* o
     return nt;
 }
 
+// Tiles, one warp per ring: the lanes fetch 32 cells' particle extents at a
+// time (cell c of ring i owns keys [(igrid_i+c)P, (igrid_i+c+1)P)), lane 0
+// packs consecutive cells greedily into tiles of at most tile_max particles
+// and at most max_span cells (shared-memory window capacity).
+__device__ int ring_tiles_warp(const Geo& g, int i, const unsigned* __restrict__ offset, int tile_max,
+                               Tile* out, int max_out, int cap_nodes, double rho_cut) {
+    const int lane = threadIdx.x & 31;
+    const int mt = __ldg(g.mtheta + i), ig = __ldg(g.igrid + i);
+    int max_span = 1;
+    if (lane == 0) {
+        if (win_nodes(g, i, 0, mt - 1, rho_cut) <= cap_nodes) {
+            max_span = mt;
+        } else {
+            int lo = 1, hi = mt - 1;
+            while (lo < hi) {
+                int mid = (lo + hi + 1) / 2;
+                if (win_nodes(g, i, 0, mid - 1, rho_cut) <= cap_nodes) lo = mid; else hi = mid - 1;
+            }
+            max_span = lo;
+        }
+    }
+    max_span = __shfl_sync(0xffffffffu, max_span, 0);
+    int nt = 0, c0 = 0;
+    long long cur = 0, tstart = offset[(long long)ig * g.P];
+    auto emit = [&](int a, int b, long long s0, long long s1) {
+        if (s1 <= s0) return;
+        if (out && nt < max_out) {
+            Tile t;
+            t.ring = i; t.c0 = a; t.c1 = b; t.pad = 0; t.start = s0; t.end = s1;
+            out[nt] = t;
+        }
+        nt++;
+    };
+    for (int cb = 0; cb < mt; cb += 32) {
+        const int cl = cb + lane;
+        long long cs_l = 0, ce_l = 0;
+        if (cl < mt) {
+            cs_l = offset[(long long)(ig + cl) * g.P];
+            ce_l = offset[(long long)(ig + cl + 1) * g.P];
+        }
+        const int nq = min(32, mt - cb);
+        for (int q = 0; q < nq; q++) {
+            const long long cs = __shfl_sync(0xffffffffu, cs_l, q);
+            const long long ce = __shfl_sync(0xffffffffu, ce_l, q);
+            if (lane != 0) continue;
+            const int c = cb + q;
+            const long long cnt = ce - cs;
+            if (cnt == 0) continue;
+            if (cur > 0 && (cur + cnt > tile_max || c - c0 + 1 > max_span)) {
+                emit(c0, c - 1 < c0 ? c0 : c - 1, tstart, cs);
+                cur = 0;
+                tstart = cs;
+                c0 = c;
+            }
+            if (cur == 0) { tstart = cs; c0 = c; }
+            cur += cnt;
+            while (cur > tile_max) {
+                emit(c0, c, tstart, tstart + tile_max);
+                tstart += tile_max;
+                cur -= tile_max;
+                c0 = c;
+            }
+        }
+    }
+    if (lane == 0 && cur > 0) emit(c0, mt - 1, tstart, tstart + cur);
+    return __shfl_sync(0xffffffffu, nt, 0);
+}
+
 __global__ void __launch_bounds__(1024) k_build_tiles(Geo g, const unsigned* __restrict__ offset, int tile_max,
                                                       Tile* tiles, int max_tiles, DevCounters* dc, int cap_nodes,
                                                       double rho_cut) {
-    __shared__ unsigned sm[32];
-    __shared__ unsigned s_carry;
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    // rings with gyrocentres: 0..mpsi-1 (bin key uses the floor ring)
-    for (int b0 = 0; b0 < g.mpsi; b0 += 1024) {
-        int i = b0 + threadIdx.x;
-        unsigned cnt = (i < g.mpsi) ? (unsigned)ring_tiles(g, i, offset, tile_max, nullptr, 0, cap_nodes, rho_cut) : 0u;
-        unsigned tot;
-        unsigned ex = block_exclusive_scan(cnt, sm, &tot) + s_carry;
-        if (i < g.mpsi) {
-            int room = max_tiles - (int)ex;
-            if (room > 0) ring_tiles(g, i, offset, tile_max, tiles + ex, room, cap_nodes, rho_cut);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) s_carry += tot;
-        __syncthreads();
+    __shared__ int ring_off[1025];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // rings with gyrocentres: 0..mpsi-1 (the bin key uses the floor ring); mpsi <= 1024
+    for (int i = warp; i < g.mpsi; i += nw) {
+        int n = ring_tiles_warp(g, i, offset, tile_max, nullptr, 0, cap_nodes, rho_cut);
+        if (lane == 0) ring_off[i] = n;
     }
-    if (threadIdx.x == 0) dc->ntiles = min((int)s_carry, max_tiles);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int i = 0; i < g.mpsi; i++) {
+            int n = ring_off[i];
+            ring_off[i] = acc;
+            acc += n;
+        }
+        ring_off[g.mpsi] = acc;
+        dc->ntiles = min(acc, max_tiles);
+    }
+    __syncthreads();
+    for (int i = warp; i < g.mpsi; i += nw) {
+        int room = max_tiles - ring_off[i];
+        if (room > 0) ring_tiles_warp(g, i, offset, tile_max, tiles + ring_off[i], room, cap_nodes, rho_cut);
+    }
 }
 
 void launch_build_tiles(const Geo& g, const unsigned* offset, int tile_max, Tile* tiles, int max_tiles,
