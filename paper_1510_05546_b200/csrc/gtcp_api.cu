@@ -88,7 +88,7 @@ struct gtcp_ctx_s {
     long long movers_sent = 0, movers_recv = 0;
     // charge config
     int charge_mode = 0;
-    int dep_ctas = 0, dep_cap_nodes = 0;
+    int dep_ctas = 0, dep_cap_nodes = 0, dep_nb = 3;
     size_t dep_smem = 0;
     // timing
     bool timing = false;
@@ -412,19 +412,23 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
-    // dynamic smem: 2 limb arrays of cap+1 words, js[(P+1) x 16] ints, column->ring bytes [cap]
-    size_t table_bytes = (size_t)(P + 1) * 16 * sizeof(int) + 64;
-    size_t per_cta = std::min<size_t>((size_t)smem_optin, 72 * 1024);
-    if (per_cta < table_bytes + 8 * 1024) {
-        c->dep_cap_nodes = 0;
-    } else {
-        c->dep_cap_nodes = (int)((per_cta - table_bytes - 16) / 9);
-        c->dep_cap_nodes &= ~3;
+    // dynamic smem: 2 limb arrays of kDepCap+1 words, row table [(P+1) x 17], column -> ring bytes
+    {
+        const char* e = getenv("GTCP_DEPOSIT_CTAS");  // 3 (default) or 2 CTAs per SM
+        c->dep_nb = (e && atoi(e) == 2) ? 2 : 3;
     }
-    c->dep_smem = (size_t)(c->dep_cap_nodes + 1) * 8 + table_bytes + c->dep_cap_nodes;
-    c->dep_ctas = nsm * 3;
-    if (P + 1 > 80 || c->dep_cap_nodes < 1024) c->charge_mode = 1;
-    else CU(configure_deposit_tiled(c->dep_smem));
+    c->dep_cap_nodes = gtcp::deposit_cap_nodes(c->dep_nb);
+    c->dep_smem = gtcp::deposit_tiled_smem(P, c->dep_nb);
+    if (c->dep_smem > (size_t)smem_optin) c->dep_cap_nodes = 0;
+    c->dep_ctas = nsm * c->dep_nb;
+    if (P + 1 > 80 || c->dep_cap_nodes < 1024) {
+        c->charge_mode = 1;
+    } else {
+        CU(configure_deposit_tiled(c->dep_smem, c->dep_nb));
+        int per_sm = gtcp::deposit_tiled_ctas_per_sm(c->dep_smem, c->dep_nb);
+        if (per_sm < 1) c->charge_mode = 1;
+        else c->dep_ctas = nsm * std::min(per_sm, c->dep_nb);
+    }
     c->launches0 = gtcp::g_launches;
     // optional: L2 persisting window on the gather field (measured: push 7% slower
     // than plain evict-first particle streams, so off by default)
@@ -624,7 +628,7 @@ static gtcp_status deposit_fx(gtcp_ctx c) {
     long long tiled_end = 0;
     if (c->charge_mode == 0 && c->n_binned > 0) {
         launch_deposit_tiled(g, s, std::min(c->n, c->n_binned), c->tiles, c->max_tiles, c->fx, c->dc, c->dep_ctas,
-                             c->dep_smem, c->dep_cap_nodes, c->st);
+                             c->dep_smem, c->dep_cap_nodes, c->dep_nb, c->st);
         tiled_end = std::min(c->n, c->n_binned);
     }
     launch_deposit_direct(g, s, tiled_end, c->n, c->fx, c->dc, c->st);

@@ -66,10 +66,15 @@ struct DevCounters {
 namespace gtcp {
 
 // ---- kernels (gtcp_kernels.cu) -------------------------------------------
+// tiled deposit, nb = CTAs per SM (3: 80 registers, 2: 128 registers and a
+// larger window); limb capacity (nodes) of one window for each
+__host__ __device__ constexpr int deposit_cap_nodes(int nb) { return nb == 2 ? 12288 : 7680; }
 void launch_deposit_tiled(const Geo& g, const PSet& s, long long n, const Tile* tiles, int max_tiles,
-                          long long* fx, DevCounters* dc, int ctas, size_t smem_bytes, int cap_nodes,
+                          long long* fx, DevCounters* dc, int ctas, size_t smem_bytes, int cap_nodes, int nb,
                           cudaStream_t st);
-cudaError_t configure_deposit_tiled(size_t smem_bytes);
+cudaError_t configure_deposit_tiled(size_t smem_bytes, int nb);
+size_t deposit_tiled_smem(int P, int nb);
+int deposit_tiled_ctas_per_sm(size_t smem_bytes, int nb);  // after configure_deposit_tiled
 void launch_deposit_direct(const Geo& g, const PSet& s, long long begin, long long n, long long* fx,
                            DevCounters* dc, cudaStream_t st);
 void launch_fx_scale(DevCounters* dc, cudaStream_t st);

@@ -295,7 +295,7 @@ __device__ __forceinline__ int win_nodes(const Geo& g, int i, int c0, int c1, do
     int h = win_halo(g, rho_cut);
     int m_lo = max(0, i - h), m_hi = min(g.mpsi, i + 1 + h);
     int S = 0;
-    for (int m = m_lo; m <= m_hi; m++) S += win_width(g, i, c0, c1, m, rho_cut);
+    for (int m = m_lo; m <= m_hi; m++) S += win_width(g, i, c0, c1, m, rho_cut) + 1;  // + trash column
     S += (16 - (S & 31) + 32) & 31;  // the plane-stride padding of k_deposit_tiled
     return S * (g.P + 1);
 }
@@ -308,6 +308,14 @@ struct WinTables {
     int mt[kMaxRings];
     long long start, end;
     int tile;
+};
+
+// per-ring constants of the tile band (index nr = the "outside the band" ring:
+// W = 0, so every contribution lands in the trash slot and is redone via L2)
+struct RingT {
+    double qt, mtd;
+    int mt, W;
+    int pad0, pad1;
 };
 
 // limbs of the fixed-point value v = round(a*b) taken straight from the bits of
@@ -323,23 +331,35 @@ __device__ __forceinline__ long long fx_val(double t) {
     return __double_as_longlong(t) - __double_as_longlong(6755399441055744.0);
 }
 
-template <class R>
-__global__ void __launch_bounds__(kDepositThreads, 3)
+// (j - js) mod mt for j, js in [0, mt): unsigned min of the two candidates
+__device__ __forceinline__ unsigned wrap_diff(int j, int js, int mt) {
+    const unsigned d = (unsigned)(j - js);
+    return min(d, d + (unsigned)mt);
+}
+
+// Shared-memory layout of k_deposit_tiled (dynamic): low limbs [kDepCap + 1]
+// (index kDepCap = trash slot), high limbs at the fixed distance kDepStride
+// (an immediate offset in the ATOMS), row table [(P+1) x kRowStride] of
+// (label window start, byte offset of the row), column -> ring bytes.
+static constexpr int kRowStride = kMaxRings + 1;
+
+template <class R, int NB>
+__global__ void __launch_bounds__(kDepositThreads, NB)
     k_deposit_tiled(Geo g, PSet s, long long n, const Tile* __restrict__ tiles, const int* ntiles_p,
                     long long* __restrict__ fx, DevCounters* dc, int cap_nodes, double rho_cut) {
+    constexpr int kDepCap = deposit_cap_nodes(NB);
+    constexpr int kDepStride = kDepCap + 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    // limbs: cap_nodes + 1 words each (the last one is a trash slot for
-    // contributions outside the window, which go to L2 instead)
     unsigned* slo = reinterpret_cast<unsigned*>(smem_raw);
-    int* shi = reinterpret_cast<int*>(slo + cap_nodes + 1);
-    int* js = shi + cap_nodes + 1;             // [(P+1) * nr] window start per (plane, ring)
-    unsigned char* colq = reinterpret_cast<unsigned char*>(js + (g.P + 1) * kMaxRings);  // [S] ring of column
+    int* shi = reinterpret_cast<int*>(slo + kDepStride);
+    int2* rowt = reinterpret_cast<int2*>(slo + 2 * kDepStride);  // 8-byte aligned: 2*kDepStride is even
+    unsigned char* colq = reinterpret_cast<unsigned char*>(rowt + (g.P + 1) * kRowStride);  // [S] ring of column
     __shared__ WinTables T;
+    __shared__ RingT RT[kMaxRings + 1];
     __shared__ unsigned long long s_fallback;
     const double scale = fx_scale(dc);
     const int ntiles = *ntiles_p;
     const int P1 = g.P + 1;
-    const int trash = cap_nodes;
     const int lane = threadIdx.x & 31;
     const int b2 = (lane >> 2) & 1, b3 = (lane >> 3) & 1, b4 = (lane >> 4) & 1;
     if (threadIdx.x == 0) s_fallback = 0;
@@ -350,60 +370,89 @@ __global__ void __launch_bounds__(kDepositThreads, 3)
         const int t = T.tile;
         if (t >= ntiles) break;
         const Tile tl = tiles[t];
-        // ---- window of this tile: rings m_lo..m_lo+nr-1, a label window per (plane, ring)
-        if (threadIdx.x == 0) {
-            int i = tl.ring;
-            int h = win_halo(g, rho_cut);
-            int m_lo = max(0, i - h), m_hi = min(g.mpsi, i + 1 + h);
-            T.m_lo = m_lo;
-            T.nr = m_hi - m_lo + 1;
-            T.start = tl.start;
-            T.end = min(tl.end, n);
-            int S = 0;
-            for (int q = 0; q < T.nr; q++) {
-                int m = m_lo + q;
-                int W = win_width(g, i, tl.c0, tl.c1, m, rho_cut);
-                T.WO[q] = make_int2(W, S);
-                T.mt[q] = __ldg(g.mtheta + m);
-                S += W;
+        // ---- window of this tile: rings m_lo..m_lo+nr-1, a label window per (plane, ring).
+        // One thread per ring computes its width, then every thread forms the
+        // (<= 16-term) column prefix itself.
+        {
+            const int i = tl.ring;
+            const int h = win_halo(g, rho_cut);
+            const int m_lo = max(0, i - h), m_hi = min(g.mpsi, i + 1 + h);
+            const int nr = m_hi - m_lo + 1;
+            if (threadIdx.x < nr) {
+                const int m = m_lo + threadIdx.x;
+                T.WO[threadIdx.x] = make_int2(win_width(g, i, tl.c0, tl.c1, m, rho_cut), 0);
+                T.mt[threadIdx.x] = __ldg(g.mtheta + m);
             }
+            __syncthreads();
+            int S = 0;
+            for (int q = 0; q < nr; q++) S += T.WO[q].x + 1;  // column W of each ring: its trash column
             // pad the plane stride to 16 (mod 32) words: the lane bit that picks
             // plane k or k+1 then always flips the shared-memory bank half
             S += (16 - (S & 31) + 32) & 31;
-            T.S = S;
-            T.total = S * P1;
-            if (T.total > cap_nodes) {  // window too large for shared memory: everything via L2
-                T.total = 0;
-                T.S = 0;
-                for (int q = 0; q < T.nr; q++) T.WO[q] = make_int2(0, 0);
+            const bool fits = S * P1 <= cap_nodes;  // else: everything via L2
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                T.m_lo = m_lo;
+                T.nr = nr;
+                T.start = tl.start;
+                T.end = min(tl.end, n);
+                T.S = fits ? S : 0;
+                T.total = fits ? S * P1 : 0;
+                int off = 0;
+                for (int q = 0; q < nr; q++) {
+                    const int W = T.WO[q].x;
+                    T.WO[q] = fits ? make_int2(W, off) : make_int2(0, 0);
+                    off += W + 1;
+                }
             }
-            for (int q = T.nr; q < kMaxRings; q++) T.WO[q] = make_int2(0, 0);
+            __syncthreads();
         }
-        __syncthreads();
         {
             const int i = tl.ring;
             const int mti = __ldg(g.mtheta + i);
             const double fc = 0.5 * (double)(tl.c0 + tl.c1 + 1) / mti;
-            for (int e = threadIdx.x; e < P1 * T.nr; e += blockDim.x) {
-                int kk = e / T.nr, q = e - kk * T.nr;
-                int m = T.m_lo + q;
-                int mt = T.mt[q];
-                double dq;
-                double hw = win_halfwidth(g, i, tl.c0, tl.c1, m, rho_cut, &dq);
-                double zk = (double)(g.k0 + kk) * g.dzeta;
-                double f = fc + zk * dq - hw;
-                f = f - floor(f);
-                DCHECK(kk * kMaxRings + q < P1 * kMaxRings);
-                js[kk * kMaxRings + q] = min(max((int)floor(f * mt), 0), mt - 1);
+            const int nr = T.nr, S = T.S;
+            for (int e = threadIdx.x; e < P1 * kRowStride; e += blockDim.x) {
+                int kk = e / kRowStride, q = e - kk * kRowStride;
+                int2 row = make_int2(0, 4 * kDepCap);  // outside the band: trash slot
+                if (q < nr && S > 0) {
+                    int m = T.m_lo + q;
+                    int mt = T.mt[q];
+                    double dq;
+                    double hw = win_halfwidth(g, i, tl.c0, tl.c1, m, rho_cut, &dq);
+                    double zk = (double)(g.k0 + kk) * g.dzeta;
+                    double f = fc + zk * dq - hw;
+                    f = f - floor(f);
+                    row.x = min(max((int)floor(f * mt), 0), mt - 1);
+                    row.y = 4 * (kk * S + T.WO[q].y);
+                } else if (q < nr) {
+                    row = make_int2(0, 4 * kDepCap);  // no window: W = 0 sends everything to the trash slot
+                }
+                rowt[e] = row;
             }
-            for (int q = 0; q < T.nr; q++)
+            if (threadIdx.x <= kMaxRings) {
+                const int q = threadIdx.x;
+                RingT rt;
+                if (q < nr) {
+                    const int m = T.m_lo + q;
+                    rt.qt = __ldg(g.qtinv + m);
+                    rt.mt = T.mt[q];
+                    rt.mtd = (double)rt.mt;
+                    rt.W = T.WO[q].x;
+                } else {
+                    rt.qt = 0.0;
+                    rt.mt = 1;
+                    rt.mtd = 1.0;
+                    rt.W = 0;
+                }
+                rt.pad0 = rt.pad1 = 0;
+                RT[q] = rt;
+            }
+            for (int x = threadIdx.x; x < S; x += blockDim.x) colq[x] = 0xFF;  // trash / padding columns
+            __syncthreads();
+            for (int q = 0; q < nr; q++)
                 for (int x = threadIdx.x; x < T.WO[q].x; x += blockDim.x) colq[T.WO[q].y + x] = (unsigned char)q;
-            // padding columns (never hit) map to the last ring; they stay zero and are skipped by the flush
             uint4* z4 = reinterpret_cast<uint4*>(slo);
-            const int nz = (2 * (cap_nodes + 1)) / 4;  // both limb arrays are contiguous
-            const int nzt = (2 * T.total + 3) / 4;
-            (void)nz;
-            // zero the used part of both limb arrays (they are not contiguous over total; do each)
             for (int e = threadIdx.x; e < (T.total + 3) / 4; e += blockDim.x) {
                 if (4 * e + 3 < T.total) {
                     z4[e] = make_uint4(0, 0, 0, 0);
@@ -412,16 +461,28 @@ __global__ void __launch_bounds__(kDepositThreads, 3)
                 }
             }
             for (int e = threadIdx.x; e < T.total; e += blockDim.x) shi[e] = 0;
-            (void)nzt;
         }
         __syncthreads();
         // ---- deposit the tile's particles (Q-1..Q-6)
-        const int m_lo = T.m_lo, nr = T.nr, S = T.S;
+        const int m_lo = T.m_lo, nr = T.nr;
         unsigned long long fb = 0;
         long long clamps = 0;
-        for (long long p = T.start + threadIdx.x; p < T.end; p += blockDim.x) {
-            const double psi = ldp_cs<R>(s.x[0], p), theta = ldp_cs<R>(s.x[1], p), zeta = ldp_cs<R>(s.x[2], p),
-                         w = ldp_cs<R>(s.x[4], p), mu = ldp_cs<R>(s.mu, p);
+        // software pipelined: the next particle's five loads are in flight
+        // while this one deposits
+        const long long pend = T.end;
+        long long p = T.start + threadIdx.x;
+        double n_psi = 0.0, n_theta = 0.0, n_zeta = 0.0, n_w = 0.0, n_mu = 0.0;
+        if (p < pend) {
+            n_psi = ldp_cs<R>(s.x[0], p); n_theta = ldp_cs<R>(s.x[1], p); n_zeta = ldp_cs<R>(s.x[2], p);
+            n_w = ldp_cs<R>(s.x[4], p); n_mu = ldp_cs<R>(s.mu, p);
+        }
+        for (; p < pend; p += blockDim.x) {
+            const double psi = n_psi, theta = n_theta, zeta = n_zeta, w = n_w, mu = n_mu;
+            const long long pn = p + blockDim.x;
+            if (pn < pend) {
+                n_psi = ldp_cs<R>(s.x[0], pn); n_theta = ldp_cs<R>(s.x[1], pn); n_zeta = ldp_cs<R>(s.x[2], pn);
+                n_w = ldp_cs<R>(s.x[4], pn); n_mu = ldp_cs<R>(s.mu, pn);
+            }
             double r, invB, rho, inv_r;
             gyro_radius(g, psi, cos(theta), mu, &r, &invB, &rho, &inv_r);
             double wz1;
@@ -433,11 +494,10 @@ __global__ void __launch_bounds__(kDepositThreads, 3)
             const double rho_r = __dmul_rn(rho, inv_r);
             // lane-rotated plane order, fixed for the whole particle: pass A uses
             // plane k + b3, pass B plane k + 1 - b3
-            const int kA = k + b3, kB = k + 1 - b3;
             const double wzA = b3 ? wzu : wzl, wzB = b3 ? wzl : wzu;
-            const int* jsA = js + kA * kMaxRings;
-            const int* jsB = js + kB * kMaxRings;
-            const int baseA = kA * S, baseB = kB * S;
+            const int2* rowA = rowt + (k + b3) * kRowStride;
+            const int2* rowB = rowt + (k + 1 - b3) * kRowStride;
+            int bad = -1;  // max over contributions of (window offset - W): >= 0 iff one hit a trash column
 #pragma unroll
             for (int lq = 0; lq < 4; lq++) {
                 // lane-rotated gyro-point: l = (lq + lane) mod 4.  r +- rho and
@@ -455,46 +515,84 @@ __global__ void __launch_bounds__(kDepositThreads, 3)
 #pragma unroll
                 for (int mq = 0; mq < 2; mq++) {
                     const int mm = mq ^ b2;  // lane-rotated ring choice
-                    const int m = ir + mm;
-                    const double qt = __ldg(g.qtinv + m);
-                    const int mt = __ldg(g.mtheta + m);
-                    double sl = __dmul_rn(__fma_rn(-zeta, qt, tl2), kInvTwoPi);
+                    const int q = ir + mm - m_lo;
+                    const int qc = (unsigned)q < (unsigned)nr ? q : nr;
+                    const RingT rt = RT[qc];
+                    double sl = __dmul_rn(__fma_rn(-zeta, rt.qt, tl2), kInvTwoPi);
                     sl = __dsub_rn(sl, floor(sl));
-                    sl = __dmul_rn(sl, (double)mt);
-                    const int j = min((int)floor(sl), mt - 1);
+                    sl = __dmul_rn(sl, rt.mtd);
+                    const int j = min((int)floor(sl), rt.mt - 1);
                     const double wt1 = __dsub_rn(sl, (double)j);
-                    const double wp = mm ? wp1 : __dsub_rn(1.0, wp1);
-                    const double a0 = __dmul_rn(__dmul_rn(0.25, wp), __dsub_rn(1.0, wt1));
-                    const double a1 = __dmul_rn(__dmul_rn(0.25, wp), wt1);
-                    const int j1 = (j + 1 == mt) ? 0 : j + 1;
-                    // node order rotated by lane bit 4: first node ja (weight aa), then jb
+                    // wp = mm ? wp1 : 1 - wp1, and the node weights rotated by lane
+                    // bit 4, each as one exact fma(+-1, x, {0, 1})
+                    const double sm = mm ? 1.0 : -1.0, s4 = b4 ? 1.0 : -1.0;
+                    const double wp = __fma_rn(sm, wp1, mm ? 0.0 : 1.0);
+                    const double qw = __dmul_rn(0.25, wp);
+                    const double aa = __dmul_rn(qw, __fma_rn(s4, wt1, b4 ? 0.0 : 1.0));
+                    const double ab = __dmul_rn(qw, __fma_rn(-s4, wt1, b4 ? 1.0 : 0.0));
+                    const int j1 = (j + 1 == rt.mt) ? 0 : j + 1;
                     const int ja = b4 ? j1 : j, jb = b4 ? j : j1;
-                    const double aa = b4 ? a1 : a0, ab = b4 ? a0 : a1;
-                    const int q = m - m_lo;
-                    const bool inr = (unsigned)q < (unsigned)nr;
-                    const int qc = inr ? q : 0;
-                    const int2 wo = T.WO[qc];
-                    const int W = inr ? wo.x : 0;
 #pragma unroll
                     for (int kq = 0; kq < 2; kq++) {
-                        const int jsv = (kq ? jsB : jsA)[qc];
-                        int da = ja - jsv, db = jb - jsv;
-                        da += (da < 0) ? mt : 0;
-                        db += (db < 0) ? mt : 0;
+                        const int2 row = (kq ? rowB : rowA)[qc];
+                        const unsigned da = wrap_diff(ja, row.x, rt.mt), db = wrap_diff(jb, row.x, rt.mt);
+                        bad = max(bad, (int)max(da, db) - rt.W);
+                        const int oa = row.y + 4 * (int)min(da, (unsigned)rt.W);
+                        const int ob = row.y + 4 * (int)min(db, (unsigned)rt.W);
                         const double wzk = kq ? wzB : wzA;
                         const double ta = fx_magic(wzk, aa), tb = fx_magic(wzk, ab);
-                        // unsigned compare: outside the band jsv belongs to another ring and d may be negative
-                        const bool oka = (unsigned)da < (unsigned)W, okb = (unsigned)db < (unsigned)W;
-                        const int base = (kq ? baseB : baseA) + wo.y;
-                        const int sa = oka ? base + da : trash, sb = okb ? base + db : trash;
-                        atomicAdd(slo + sa, fx_lo(ta));
-                        atomicAdd(shi + sa, fx_hi(ta));
-                        atomicAdd(slo + sb, fx_lo(tb));
-                        atomicAdd(shi + sb, fx_hi(tb));
-                        if (__builtin_expect(!(oka && okb), 0)) {
-                            const int kp = kq ? kB : kA;
-                            if (!oka) { long long v = fx_val(ta); if (v) { red_i64(fx + fx_node(g, kp, m, ja, mt), v); fb++; } }
-                            if (!okb) { long long v = fx_val(tb); if (v) { red_i64(fx + fx_node(g, kp, m, jb, mt), v); fb++; } }
+                        unsigned char* base = reinterpret_cast<unsigned char*>(slo);
+                        atomicAdd(reinterpret_cast<unsigned*>(base + oa), fx_lo(ta));
+                        atomicAdd(reinterpret_cast<int*>(base + oa + 4 * kDepStride), fx_hi(ta));
+                        atomicAdd(reinterpret_cast<unsigned*>(base + ob), fx_lo(tb));
+                        atomicAdd(reinterpret_cast<int*>(base + ob + 4 * kDepStride), fx_hi(tb));
+                    }
+                }
+            }
+            if (__builtin_expect(bad >= 0, 0)) {
+                // rare: some contributions fell outside the tile window (trash
+                // columns).  Redo exactly those, with the same arithmetic, into L2.
+                const int kp0 = k + b3, kp1 = k + 1 - b3;
+#pragma unroll 1
+                for (int lq = 0; lq < 4; lq++) {
+                    const int l = (lq + lane) & 3;
+                    const double sr = (double)(((l + 1) & 1) * (1 - (l & 2)));
+                    const double stt = (double)((l & 1) * (1 - (l & 2)));
+                    double rl = __fma_rn(sr, rho, r);
+                    const double tl2 = __fma_rn(stt, rho_r, theta);
+                    rl = fmin(fmax(rl, g.a0), g.a1);
+                    const double x = __dmul_rn(__dsub_rn(rl, g.a0), g.inv_dr);
+                    const int ir = min(max((int)floor(x), 0), g.mpsi - 1);
+                    const double wp1 = __dsub_rn(x, (double)ir);
+#pragma unroll 1
+                    for (int mm = 0; mm < 2; mm++) {
+                        const int m = ir + mm, q = m - m_lo;
+                        const int qc = (unsigned)q < (unsigned)nr ? q : nr;
+                        const RingT rt = RT[qc];
+                        const double qt = __ldg(g.qtinv + m);
+                        const int mt = __ldg(g.mtheta + m);
+                        double sl = __dmul_rn(__fma_rn(-zeta, qt, tl2), kInvTwoPi);
+                        sl = __dsub_rn(sl, floor(sl));
+                        sl = __dmul_rn(sl, (double)mt);
+                        const int j = min((int)floor(sl), mt - 1);
+                        const double wt1 = __dsub_rn(sl, (double)j);
+                        const double wp = mm ? wp1 : __dsub_rn(1.0, wp1);
+                        const double qw = __dmul_rn(0.25, wp);
+                        const double a0 = __dmul_rn(qw, __dsub_rn(1.0, wt1)), a1 = __dmul_rn(qw, wt1);
+                        const int j1 = (j + 1 == mt) ? 0 : j + 1;
+#pragma unroll 1
+                        for (int kq = 0; kq < 2; kq++) {
+                            const int2 row = (kq ? rowB : rowA)[qc];
+                            const double wzk = kq ? wzB : wzA;
+#pragma unroll 1
+                            for (int u = 0; u < 2; u++) {
+                                const int ju = u ? j1 : j;
+                                // same test as the fast path: in the band and inside the window
+                                const bool in = qc < nr && wrap_diff(ju, row.x, rt.mt) < (unsigned)rt.W;
+                                if (in) continue;
+                                const long long v = fx_val(fx_magic(wzk, u ? a1 : a0));
+                                if (v) { red_i64(fx + fx_node(g, kq ? kp1 : kp0, m, ju, mt), v); fb++; }
+                            }
                         }
                     }
                 }
@@ -504,19 +602,21 @@ __global__ void __launch_bounds__(kDepositThreads, 3)
         if (clamps) atomicAdd((unsigned long long*)&dc->plane_clamps, (unsigned long long)clamps);
         __syncthreads();
         // ---- flush the window to L2 (one REDG.ADD.64 per nonzero node)
+        const int S = T.S;
         if (S > 0) {
             int kk = threadIdx.x / S, x = threadIdx.x - kk * S;
             const int bdiv = blockDim.x / S, bmod = blockDim.x - bdiv * S;
             for (int e = threadIdx.x; e < T.total; e += blockDim.x) {
-                long long v = (long long)shi[e] * (1LL << kLimbBits) + (long long)slo[e];
-                if (v != 0) {
-                    DCHECK(x >= 0 && x < S && kk >= 0 && kk < P1);
-                    const int q = colq[x];
-                    DCHECK(q < nr);
-                    const int mt = T.mt[q];
-                    int j = js[kk * kMaxRings + q] + (x - T.WO[q].y);
-                    if (j >= mt) j -= mt;
-                    red_i64(fx + fx_node(g, kk, m_lo + q, j, mt), v);
+                const int q = colq[x];
+                if (q != 0xFF) {
+                    long long v = (long long)shi[e] * (1LL << kLimbBits) + (long long)slo[e];
+                    if (v != 0) {
+                        DCHECK(x >= 0 && x < S && kk >= 0 && kk < P1 && q < nr);
+                        const int mt = T.mt[q];
+                        int j = rowt[kk * kRowStride + q].x + (x - T.WO[q].y);
+                        if (j >= mt) j -= mt;
+                        red_i64(fx + fx_node(g, kk, m_lo + q, j, mt), v);
+                    }
                 }
                 x += bmod;
                 kk += bdiv;
@@ -528,24 +628,46 @@ __global__ void __launch_bounds__(kDepositThreads, 3)
     if (threadIdx.x == 0 && s_fallback) atomicAdd((unsigned long long*)&dc->fallback, s_fallback);
 }
 
-cudaError_t configure_deposit_tiled(size_t smem_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(k_deposit_tiled<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <int NB>
+static cudaError_t configure_nb(size_t smem_bytes) {
+    cudaError_t e = cudaFuncSetAttribute(k_deposit_tiled<double, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem_bytes);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_deposit_tiled<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+    return cudaFuncSetAttribute(k_deposit_tiled<float, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem_bytes);
+}
+
+cudaError_t configure_deposit_tiled(size_t smem_bytes, int nb) {
+    return nb == 2 ? configure_nb<2>(smem_bytes) : configure_nb<3>(smem_bytes);
+}
+
+int deposit_tiled_ctas_per_sm(size_t smem_bytes, int nb) {
+    int r = 0;
+    cudaError_t e = nb == 2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_deposit_tiled<double, 2>,
+                                                                          kDepositThreads, smem_bytes)
+                            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_deposit_tiled<double, 3>,
+                                                                          kDepositThreads, smem_bytes);
+    return e == cudaSuccess ? r : 0;
+}
+
+size_t deposit_tiled_smem(int P, int nb) {
+    const int cap = deposit_cap_nodes(nb);
+    return (size_t)(2 * (cap + 1)) * 4 + (size_t)(P + 1) * kRowStride * 8 + (size_t)(cap / (P + 1) + 64);
 }
 
 void launch_deposit_tiled(const Geo& g, const PSet& s, long long n, const Tile* tiles, int max_tiles,
-                          long long* fx, DevCounters* dc, int ctas, size_t smem_bytes, int cap_nodes,
+                          long long* fx, DevCounters* dc, int ctas, size_t smem_bytes, int cap_nodes, int nb,
                           cudaStream_t st) {
     (void)max_tiles;
     double rho_cut = deposit_rho_cut(g);
-    if (g.prec32)
-        k_deposit_tiled<float><<<ctas, kDepositThreads, smem_bytes, st>>>(g, s, n, tiles, &dc->ntiles, fx, dc,
-                                                                          cap_nodes, rho_cut);
-    else
-        k_deposit_tiled<double><<<ctas, kDepositThreads, smem_bytes, st>>>(g, s, n, tiles, &dc->ntiles, fx, dc,
-                                                                           cap_nodes, rho_cut);
+#define GTCP_DEP(RT, NBV) \
+    k_deposit_tiled<RT, NBV><<<ctas, kDepositThreads, smem_bytes, st>>>(g, s, n, tiles, &dc->ntiles, fx, dc, cap_nodes, rho_cut)
+    if (g.prec32) {
+        if (nb == 2) GTCP_DEP(float, 2); else GTCP_DEP(float, 3);
+    } else {
+        if (nb == 2) GTCP_DEP(double, 2); else GTCP_DEP(double, 3);
+    }
+#undef GTCP_DEP
     g_launches++;
 }
 
