@@ -23,9 +23,12 @@ def sources():
         [os.path.join(ROOT, "include", "gtcp.h")]
 
 
-def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug: bool = False, defines=(), out: str | None = None) -> str:
+    """defines / out: experiment builds (extra -D flags into another .so)."""
     srcs = sources()
     LIB = globals()["LIB"] if not debug else os.path.join(HERE, "_lib", "libgtcp_debug.so")
+    if out:
+        LIB = out
     if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(s) for s in srcs):
         return LIB
     inc, lib = nccl_dirs()
@@ -36,7 +39,7 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
            "-I", os.path.join(ROOT, "include"), "-I", inc,
            "-o", tmp] + [s for s in srcs if s.endswith(".cu")] + \
           ["-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib] + \
-          (["-DGTCP_DEBUG"] if debug else [])
+          (["-DGTCP_DEBUG"] if debug else []) + ["-D" + d for d in defines]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
@@ -48,4 +51,7 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv or bool(defs), verbose="-v" in sys.argv, debug="--debug" in sys.argv,
+                defines=defs, out=outs[0] if outs else None))

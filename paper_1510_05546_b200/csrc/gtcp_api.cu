@@ -51,6 +51,7 @@ struct gtcp_ctx_s {
     unsigned *key = nullptr, *rankbuf = nullptr, *count = nullptr, *offset = nullptr, *scan_tmp = nullptr;
     Tile* tiles = nullptr;
     int max_tiles = 0;
+    int* tile_span = nullptr;  // per ring: widest cell span whose window fits smem; then per-ring tile counts
     long long n_binned = 0;  // particles [0, n_binned) are covered by tiles
     int tile_max = 8192;  // <= 8192: bounds the smem limb sums (gtcp_kernels.cu smem_add)
     // grids
@@ -375,6 +376,7 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     CU(dalloc(&c->scan_tmp, (c->nkeys + 4095) / 4096 + 1));
     c->max_tiles = (int)std::min<long long>((long long)mg + c->cap / 1024 + M + 16, 1LL << 30);
     CU(dalloc(&c->tiles, c->max_tiles));
+    CU(dalloc(&c->tile_span, 2LL * M));  // [M] max label span per ring, [M] tiles per ring
     // grids
     long long HP = (long long)(P + 3) * mg;
     CU(dalloc(&c->fx, (long long)(P + 1) * mg));
@@ -429,6 +431,7 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
         if (per_sm < 1) c->charge_mode = 1;
         else c->dep_ctas = nsm * std::min(per_sm, c->dep_nb);
     }
+    gtcp::launch_tile_spans(c->geo, c->dep_cap_nodes, c->tile_span, c->st);
     c->launches0 = gtcp::g_launches;
     // optional: L2 persisting window on the gather field (measured: push 7% slower
     // than plain evict-first particle streams, so off by default)
@@ -499,7 +502,7 @@ extern "C" void gtcp_destroy(gtcp_ctx c) {
     // the live/saved/mu/scratch pointers are always a permutation of the original allocations
     for (int d = 0; d < 5; d++) { F(c->live[d]); F(c->saved[d]); }
     F(c->mu); F(c->scratch); F(c->id); F(c->id_scratch);
-    F(c->key); F(c->rankbuf); F(c->count); F(c->offset); F(c->scan_tmp); F(c->tiles);
+    F(c->key); F(c->rankbuf); F(c->count); F(c->offset); F(c->scan_tmp); F(c->tiles); F(c->tile_span);
     F(c->fx); F(c->rhoH); F(c->dnH); F(c->tmpH); F(c->phiH); F(c->rhs); F(c->jphi); F(c->g1); F(c->g2);
     F(c->gfield); F(c->nm); F(c->ringsum); F(c->phi00); F(c->halo_buf); F(c->fx_recv); F(c->dc); F(c->d_scalar); F(c->d_partial);
     F(c->d_mtheta); F(c->d_igrid); F(c->d_itran); F(c->d_qtinv); F(c->d_node_ring);
@@ -864,7 +867,8 @@ static gtcp_status do_bin(gtcp_ctx c) {
             std::swap(c->id, c->id_scratch);
         }
     }
-    launch_build_tiles(g, c->offset, c->tile_max, c->tiles, c->max_tiles, c->dc, c->dep_cap_nodes, c->st);
+    launch_build_tiles(g, c->offset, c->tile_max, c->tiles, c->max_tiles, c->dc, c->tile_span,
+                       c->tile_span + c->geo.mpsi, c->st);
     c->n_binned = c->n;
     KCHECK();
     return GTCP_OK;

@@ -104,7 +104,8 @@ void launch_permute_f64(const double* src, double* dst, const unsigned* dest, lo
 void launch_permute_u64(const unsigned long long* src, unsigned long long* dst, const unsigned* dest,
                         long long n, cudaStream_t st);
 void launch_build_tiles(const Geo& g, const unsigned* offset, int tile_max, Tile* tiles, int max_tiles,
-                        DevCounters* dc, int cap_nodes, cudaStream_t st);
+                        DevCounters* dc, const int* span, int* ring_cnt, cudaStream_t st);
+void launch_tile_spans(const Geo& g, int cap_nodes, int* span, cudaStream_t st);  // once, at init
 void launch_load(const Geo& g, const PSet& s, long long n, unsigned long long seed, long long id0,
                  double w_amp, double vcut, double zlo, double zhi, double rlo, double rhi, cudaStream_t st);
 // grid kernels (gtcp_grid.cu)

@@ -1652,28 +1652,42 @@ __device__ __forceinline__ int ring_tiles(const Geo& g, int i, const unsigned* o
     return nt;
 }
 
-// Tiles, one warp per ring: the lanes fetch 32 cells' particle extents at a
-// time (cell c of ring i owns keys [(igrid_i+c)P, (igrid_i+c+1)P)), lane 0
-// packs consecutive cells greedily into tiles of at most tile_max particles
-// and at most max_span cells (shared-memory window capacity).
+// Tiles.  max_span[i] = the widest label-cell span of ring i whose window
+// (all planes, radial band, label windows) fits the shared-memory capacity;
+// a geometry constant, computed once at init by a 32-ary search (one
+// candidate span per lane).
+__global__ void k_tile_spans(Geo g, int cap_nodes, double rho_cut, int* __restrict__ span) {
+    const int lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= g.mpsi) return;
+    const int mt = __ldg(g.mtheta + i);
+    int lo = 1, hi = mt;  // answer in [lo, hi]; span 1 assumed to fit (else one-cell tiles go via L2)
+    while (lo < hi) {
+        const int c = lo + (int)(((long long)(hi - lo) * (lane + 1) + 31) / 32);  // in (lo, hi]
+        const bool fits = win_nodes(g, i, 0, c - 1, rho_cut) <= cap_nodes;
+        const unsigned fm = __ballot_sync(0xffffffffu, fits), nm = __ballot_sync(0xffffffffu, !fits);
+        // candidates increase with the lane: the fitting ones form a prefix
+        const int nlo = fm ? __shfl_sync(0xffffffffu, c, 31 - __clz(fm)) : lo;
+        const int nhi = nm ? __shfl_sync(0xffffffffu, c, __ffs(nm) - 1) - 1 : hi;
+        lo = nlo;
+        hi = nhi;
+    }
+    if (lane == 0) span[i] = lo;
+}
+
+void launch_tile_spans(const Geo& g, int cap_nodes, int* span, cudaStream_t st) {
+    k_tile_spans<<<(g.mpsi + 3) / 4, 128, 0, st>>>(g, cap_nodes, deposit_rho_cut(g), span);
+    g_launches++;
+}
+
+// One warp per ring: the lanes fetch 32 cells' particle extents at a time
+// (cell c of ring i owns keys [(igrid_i+c)P, (igrid_i+c+1)P)), lane 0 packs
+// consecutive cells greedily into tiles of at most tile_max particles and at
+// most max_span cells.  Returns the ring's tile count (written if out).
 __device__ int ring_tiles_warp(const Geo& g, int i, const unsigned* __restrict__ offset, int tile_max,
-                               Tile* out, int max_out, int cap_nodes, double rho_cut) {
+                               int max_span, Tile* out, int max_out) {
     const int lane = threadIdx.x & 31;
     const int mt = __ldg(g.mtheta + i), ig = __ldg(g.igrid + i);
-    int max_span = 1;
-    if (lane == 0) {
-        if (win_nodes(g, i, 0, mt - 1, rho_cut) <= cap_nodes) {
-            max_span = mt;
-        } else {
-            int lo = 1, hi = mt - 1;
-            while (lo < hi) {
-                int mid = (lo + hi + 1) / 2;
-                if (win_nodes(g, i, 0, mid - 1, rho_cut) <= cap_nodes) lo = mid; else hi = mid - 1;
-            }
-            max_span = lo;
-        }
-    }
-    max_span = __shfl_sync(0xffffffffu, max_span, 0);
     int nt = 0, c0 = 0;
     long long cur = 0, tstart = offset[(long long)ig * g.P];
     auto emit = [&](int a, int b, long long s0, long long s1) {
@@ -1687,7 +1701,7 @@ __device__ int ring_tiles_warp(const Geo& g, int i, const unsigned* __restrict__
     };
     for (int cb = 0; cb < mt; cb += 32) {
         const int cl = cb + lane;
-        long long cs_l = 0, ce_l = 0;
+        unsigned cs_l = 0, ce_l = 0;
         if (cl < mt) {
             cs_l = offset[(long long)(ig + cl) * g.P];
             ce_l = offset[(long long)(ig + cl + 1) * g.P];
@@ -1720,38 +1734,36 @@ __device__ int ring_tiles_warp(const Geo& g, int i, const unsigned* __restrict__
     return __shfl_sync(0xffffffffu, nt, 0);
 }
 
-__global__ void __launch_bounds__(1024) k_build_tiles(Geo g, const unsigned* __restrict__ offset, int tile_max,
-                                                      Tile* tiles, int max_tiles, DevCounters* dc, int cap_nodes,
-                                                      double rho_cut) {
-    __shared__ int ring_off[1025];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    // rings with gyrocentres: 0..mpsi-1 (the bin key uses the floor ring); mpsi <= 1024
-    for (int i = warp; i < g.mpsi; i += nw) {
-        int n = ring_tiles_warp(g, i, offset, tile_max, nullptr, 0, cap_nodes, rho_cut);
-        if (lane == 0) ring_off[i] = n;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int i = 0; i < g.mpsi; i++) {
-            int n = ring_off[i];
-            ring_off[i] = acc;
-            acc += n;
-        }
-        ring_off[g.mpsi] = acc;
-        dc->ntiles = min(acc, max_tiles);
-    }
-    __syncthreads();
-    for (int i = warp; i < g.mpsi; i += nw) {
-        int room = max_tiles - ring_off[i];
-        if (room > 0) ring_tiles_warp(g, i, offset, tile_max, tiles + ring_off[i], room, cap_nodes, rho_cut);
-    }
+// pass 1: tile count per ring (rings with gyrocentres: 0..mpsi-1, the bin key
+// uses the floor ring), one warp per ring spread over the SMs
+__global__ void k_tiles_count(Geo g, const unsigned* __restrict__ offset, int tile_max, const int* __restrict__ span,
+                              int* __restrict__ ring_cnt) {
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= g.mpsi) return;
+    const int n = ring_tiles_warp(g, i, offset, tile_max, span[i], nullptr, 0);
+    if ((threadIdx.x & 31) == 0) ring_cnt[i] = n;
+}
+
+// pass 2: each warp sums the counts of the rings before its own, then writes
+__global__ void k_tiles_write(Geo g, const unsigned* __restrict__ offset, int tile_max, const int* __restrict__ span,
+                              const int* __restrict__ ring_cnt, Tile* tiles, int max_tiles, DevCounters* dc) {
+    const int lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= g.mpsi) return;
+    int acc = 0;
+    for (int q = lane; q < i; q += 32) acc += ring_cnt[q];
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    const int room = max_tiles - acc;
+    if (room > 0) ring_tiles_warp(g, i, offset, tile_max, span[i], tiles + acc, room);
+    if (i == g.mpsi - 1 && lane == 0) dc->ntiles = min(acc + ring_cnt[i], max_tiles);
 }
 
 void launch_build_tiles(const Geo& g, const unsigned* offset, int tile_max, Tile* tiles, int max_tiles,
-                        DevCounters* dc, int cap_nodes, cudaStream_t st) {
-    k_build_tiles<<<1, 1024, 0, st>>>(g, offset, tile_max, tiles, max_tiles, dc, cap_nodes, deposit_rho_cut(g));
-    g_launches++;
+                        DevCounters* dc, const int* span, int* ring_cnt, cudaStream_t st) {
+    const int blocks = (g.mpsi + 3) / 4;
+    k_tiles_count<<<blocks, 128, 0, st>>>(g, offset, tile_max, span, ring_cnt);
+    k_tiles_write<<<blocks, 128, 0, st>>>(g, offset, tile_max, span, ring_cnt, tiles, max_tiles, dc);
+    g_launches += 2;
 }
 
 // deterministic sum: fixed grid of partials, then one block in fixed order
