@@ -828,13 +828,9 @@ static gtcp_status do_bin(gtcp_ctx c) {
     launch_bin_keys(g, s, c->n, c->key, c->rankbuf, c->count, c->st);
     launch_scan_u32(c->count, c->offset, c->nkeys, c->scan_tmp, c->st);
     launch_bin_dest(c->key, c->rankbuf, c->offset, c->n, c->rankbuf, c->st);
-    // scatter form (no inverse pass) measured 40% slower than the gather form
-    static const bool scatter = [] {
-        const char* e = getenv("GTCP_BIN_SCATTER");
-        return e && e[0] == '1';
-    }();
     // gather form: inv[dest[p]] = p once, then every array is written coalesced
-    if (!scatter) launch_perm_inverse(c->rankbuf, c->n, c->key, c->st);
+    // (scatter forms measured slower: plain 40 %, smem-staged chunks 7 %)
+    launch_perm_inverse(c->rankbuf, c->n, c->key, c->st);
     // permute live state, mu (and the saved state when mid-step) in one fused
     // gather pass into the other ping-pong set + spare arrays, then swap pointers
     std::vector<double**> arrs;
@@ -849,13 +845,11 @@ static gtcp_status do_bin(gtcp_ctx c) {
         for (int d = 0; d < 5; d++) { src[d] = c->live[d]; dst[d] = c->saved[d]; }
         src[5] = c->mu;
         dst[5] = c->scratch;
-        if (scatter) launch_scatter_perm_multi(src, dst, 6, c->id, c->id ? c->id_scratch : nullptr, c->rankbuf, c->n, c->st);
-        else launch_gather_perm_multi(src, dst, 6, c->id, c->id ? c->id_scratch : nullptr, c->key, c->n, c->st);
+        launch_gather_perm_multi(src, dst, 6, c->id, c->id ? c->id_scratch : nullptr, c->key, c->n, c->st);
         for (int d = 0; d < 5; d++) std::swap(c->live[d], c->saved[d]);
         std::swap(c->mu, c->scratch);
         if (c->id) std::swap(c->id, c->id_scratch);
     } else {
-        if (scatter) launch_perm_inverse(c->rankbuf, c->n, c->key, c->st);  // mid-step (rare): gather form
         for (double** a : arrs) {
             launch_gather_perm_f64(*a, c->scratch, c->key, c->n, c->st);
             double* old = *a;

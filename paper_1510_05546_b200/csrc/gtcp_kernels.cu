@@ -91,53 +91,6 @@ __device__ __forceinline__ void gyro_stencil(const Geo& g, double r, double thet
     }
 }
 
-// Lane-rotated variant for the shared-memory scatter.  The 32 contributions
-// of a particle are indexed by (l, mm, kk, jj) = (point, ring, plane, node);
-// at every step lane b visits slot (l, mm, kk, jj) XOR its lane bits, so the
-// 32 lanes of a warp (cell-sorted, i.e. neighbouring particles) touch 32
-// different (point, ring, plane, node) slots instead of colliding on the same
-// shared-memory word.  Arithmetic is bit-identical to gyro_stencil.
-// fn(m, j, mt, kk, a0, a1): nodes j and j+1 (j+1 may be mt = the duplicate).
-template <class Fn>
-__device__ __forceinline__ void gyro_stencil_rot(const Geo& g, double r, double theta, double zeta, double rho,
-                                                 double inv_r, int lane, Fn&& fn) {
-    const double rho_r = __dmul_rn(rho, inv_r);
-#pragma unroll
-    for (int lq = 0; lq < 4; lq++) {
-        const int l = (lq + lane) & 3;
-        double rl = r, tl = theta;
-        if (l == 0) rl = __dadd_rn(r, rho);
-        if (l == 2) rl = __dsub_rn(r, rho);
-        if (l == 1) tl = __dadd_rn(theta, rho_r);
-        if (l == 3) tl = __dsub_rn(theta, rho_r);
-        rl = fmin(fmax(rl, g.a0), g.a1);
-        double x = __dmul_rn(__dsub_rn(rl, g.a0), g.inv_dr);
-        int i = (int)floor(x);
-        i = min(max(i, 0), g.mpsi - 1);
-        double wp1 = __dsub_rn(x, (double)i);
-#pragma unroll
-        for (int mq = 0; mq < 2; mq++) {
-            const int mm = mq ^ ((lane >> 2) & 1);
-            int m = i + mm;
-            double qt = __ldg(g.qtinv + m);
-            int mt = __ldg(g.mtheta + m);
-            double s = __dmul_rn(__fma_rn(-zeta, qt, tl), kInvTwoPi);
-            s = __dsub_rn(s, floor(s));
-            s = __dmul_rn(s, (double)mt);
-            int j = min((int)floor(s), mt - 1);
-            double wt1 = __dsub_rn(s, (double)j);
-            double wp = mm ? wp1 : __dsub_rn(1.0, wp1);
-            double a0 = __dmul_rn(__dmul_rn(0.25, wp), __dsub_rn(1.0, wt1));
-            double a1 = __dmul_rn(__dmul_rn(0.25, wp), wt1);
-#pragma unroll
-            for (int kq = 0; kq < 2; kq++) {
-                const int kk = kq ^ ((lane >> 3) & 1);
-                fn(m, j, mt, kk, a0, a1);
-            }
-        }
-    }
-}
-
 // per-particle gyroradius inputs with explicit roundings (shared by all kernels)
 __device__ __forceinline__ void gyro_radius(const Geo& g, double psi, double ct, double mu, double* r, double* invB,
                                             double* rho, double* inv_r) {
@@ -1499,40 +1452,6 @@ __global__ void k_gather_perm_multi(PermArrays A, const unsigned* __restrict__ i
     }
 }
 
-// scatter form: dst_a[dest[p]] = src_a[p] (coalesced reads; on nearly sorted
-// input the writes come in runs)
-template <class R>
-__global__ void k_scatter_perm_multi(PermArrays A, const unsigned* __restrict__ dest, long long n) {
-    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-         p += (long long)gridDim.x * blockDim.x) {
-        const long long d = dest[p];
-        R v[12];
-#pragma unroll
-        for (int a = 0; a < 12; a++)
-            if (a < A.na) v[a] = __ldcs(reinterpret_cast<const R*>(A.src[a]) + p);
-#pragma unroll
-        for (int a = 0; a < 12; a++)
-            if (a < A.na) reinterpret_cast<R*>(A.dst[a])[d] = v[a];
-        if (A.id_src) A.id_dst[d] = A.id_src[p];
-    }
-}
-
-void launch_scatter_perm_multi(const double* const* src, double* const* dst, int na, const unsigned long long* id_src,
-                               unsigned long long* id_dst, const unsigned* dest, long long n, cudaStream_t st) {
-    if (n <= 0) return;
-    PermArrays A;
-    for (int a = 0; a < 12; a++) {
-        A.src[a] = a < na ? src[a] : nullptr;
-        A.dst[a] = a < na ? dst[a] : nullptr;
-    }
-    A.na = na;
-    A.id_src = id_src;
-    A.id_dst = id_dst;
-    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
-    if (g_prec32) k_scatter_perm_multi<float><<<blocks, 256, 0, st>>>(A, dest, n);
-    else k_scatter_perm_multi<double><<<blocks, 256, 0, st>>>(A, dest, n);
-    g_launches++;
-}
 
 void launch_gather_perm_multi(const double* const* src, double* const* dst, int na, const unsigned long long* id_src,
                               unsigned long long* id_dst, const unsigned* inv, long long n, cudaStream_t st) {
