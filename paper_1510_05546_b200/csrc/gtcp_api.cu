@@ -328,6 +328,8 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     g.R0 = p->R0; g.inv_R0 = 1.0 / p->R0; g.omega0 = p->omega0; g.q0 = p->q0; g.q2 = p->q2;
     g.rln = p->rln; g.rlt = p->rlt; g.tau = p->tau; g.dt = p->dt;
     g.cz = p->mzetamax / GTCP_TWO_PI;
+    g.psi_lo = 0.5 * g.a0 * g.a0 * (1.0 + 1e-12);
+    g.psi_hi = 0.5 * g.a1 * g.a1 * (1.0 - 1e-12);
     g.dzeta = GTCP_TWO_PI / p->mzetamax;
     g.rhoG = std::sqrt(2.0) / p->omega0;
     g.inv_omega0 = 1.0 / p->omega0;

@@ -33,6 +33,14 @@ long long g_launches = 0;
 int g_prec32 = 0;  // precision of the particle store of the context being driven (set per call)
 
 static constexpr double kInvTwoPi = 1.0 / GTCP_TWO_PI;
+static constexpr double kInvPi = 2.0 / GTCP_TWO_PI;
+
+// theta is kept in [0, 2 pi) (U-8 wrap), so sin/cos go through the pi-scaled
+// forms: exact argument reduction, no large-argument path (about half the
+// instructions of sincos(theta)); the one rounding of theta/pi is far below
+// the P-0 tolerance.
+__device__ __forceinline__ double cos_theta(double theta) { return cospi(theta * kInvPi); }
+__device__ __forceinline__ void sincos_theta(double theta, double* s, double* c) { sincospi(theta * kInvPi, s, c); }
 static constexpr int kMaxRings = 16;   // radial band of one tile window
 static constexpr int kDepositThreads = 256;
 
@@ -184,7 +192,7 @@ __global__ void __launch_bounds__(256) k_deposit_direct(Geo g, PSet s, long long
         double psi = ldp<R>(s.x[0], p), theta = ldp<R>(s.x[1], p), zeta = ldp<R>(s.x[2], p), w = ldp<R>(s.x[4], p),
                mu = ldp<R>(s.mu, p);
         double r, invB, rho, inv_r;
-        gyro_radius(g, psi, cos(theta), mu, &r, &invB, &rho, &inv_r);
+        gyro_radius(g, psi, cos_theta(theta), mu, &r, &invB, &rho, &inv_r);
         double wz1;
         int kg = plane_of(g, zeta, &wz1);
         int k = kg - g.k0;
@@ -437,7 +445,7 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
                 n_w = ldp_cs<R>(s.x[4], pn); n_mu = ldp_cs<R>(s.mu, pn);
             }
             double r, invB, rho, inv_r;
-            gyro_radius(g, psi, cos(theta), mu, &r, &invB, &rho, &inv_r);
+            gyro_radius(g, psi, cos_theta(theta), mu, &r, &invB, &rho, &inv_r);
             double wz1;
             const int kg = plane_of(g, zeta, &wz1);
             int k = kg - g.k0;
@@ -716,7 +724,7 @@ __device__ __forceinline__ void push_one(const Geo& g, const RingTab* __restrict
                                          long long& clamps, const Fetch* fetch = nullptr) {
     // U-1
     double st, ct;
-    sincos(theta, &st, &ct);
+    sincos_theta(theta, &st, &ct);
     double r, invB, rho, inv_r;
     gyro_radius(g, psi, ct, mu, &r, &invB, &rho, &inv_r);
     const double eps = r * g.inv_R0;
@@ -834,11 +842,15 @@ __device__ __forceinline__ void push_one(const Geo& g, const RingTab* __restrict
             X[d] = t;
         }
     }
-    double rn = sqrt(2.0 * fmax(X[0], 0.0));
-    bool rf = false;
-    if (rn > g.a1) { rn = 2.0 * g.a1 - rn; rf = true; }
-    if (rn < g.a0) { rn = 2.0 * g.a0 - rn; rf = true; }
-    if (rf) { X[0] = 0.5 * rn * rn; refl++; }
+    // r = sqrt(2 psi) only when it may leave [a0, a1] (psi bounds padded by a
+    // few ulps; the decision itself is taken on r as in the oracle)
+    if (!(X[0] > g.psi_lo && X[0] < g.psi_hi)) {
+        double rn = sqrt(2.0 * fmax(X[0], 0.0));
+        bool rf = false;
+        if (rn > g.a1) { rn = 2.0 * g.a1 - rn; rf = true; }
+        if (rn < g.a0) { rn = 2.0 * g.a0 - rn; rf = true; }
+        if (rf) { X[0] = 0.5 * rn * rn; refl++; }
+    }
 }
 
 __device__ __forceinline__ void push_epilogue(DevCounters* dc, double wmax, long long refl, long long clamps,
@@ -868,7 +880,8 @@ __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long lon
         for (int d = 0; d < 5; d++) base[d] = ld(pp.base[d]);
         push_one<GU>(g, rt_dyn, ld(pp.src[0]), ld(pp.src[1]), ld(pp.src[2]), ld(pp.src[3]), ld(pp.src[4]), ld(pp.mu),
                  base, h, gf, X, refl, clamps);
-        if (!(isfinite(X[0]) && isfinite(X[1]) && isfinite(X[2]) && isfinite(X[3]) && isfinite(X[4]))) nonfinite = 1;
+        // one test: a NaN or Inf in any component survives the product with 0
+        if (!isfinite((X[0] + X[1] + X[2] + X[3]) * 0.0 + X[4])) nonfinite = 1;
 #pragma unroll
         for (int d = 0; d < 5; d++) {
             if (CS) stp_cs<R>(pp.out[d], p, X[d]);
