@@ -1530,60 +1530,6 @@ void launch_permute_u64(const unsigned long long* src, unsigned long long* dst, 
     g_launches++;
 }
 
-// Tiles: one thread per ring walks its cells (cell extent from the key
-// offsets: cell c of ring i owns keys [(igrid_i+c)P, (igrid_i+c+1)P)) and
-// greedily packs consecutive cells into tiles of at most tile_max particles.
-__device__ __forceinline__ int ring_tiles(const Geo& g, int i, const unsigned* offset, int tile_max,
-                                          Tile* out, int max_out, int cap_nodes, double rho_cut) {
-    int mt = __ldg(g.mtheta + i), ig = __ldg(g.igrid + i);
-    int nt = 0;
-    // largest label span whose window fits the shared-memory capacity
-    int max_span = 1;
-    if (win_nodes(g, i, 0, mt - 1, rho_cut) <= cap_nodes) {
-        max_span = mt;
-    } else {
-        int lo = 1, hi = mt - 1;  // win_nodes(span lo) assumed to fit (else one-cell tiles go via L2)
-        while (lo < hi) {
-            int mid = (lo + hi + 1) / 2;
-            if (win_nodes(g, i, 0, mid - 1, rho_cut) <= cap_nodes) lo = mid; else hi = mid - 1;
-        }
-        max_span = lo;
-    }
-    long long cur = 0, tstart = offset[(long long)ig * g.P];
-    int c0 = 0;
-    auto emit = [&](int a, int b, long long s0, long long s1) {
-        if (s1 <= s0) return;
-        if (out && nt < max_out) {
-            Tile t;
-            t.ring = i; t.c0 = a; t.c1 = b; t.pad = 0; t.start = s0; t.end = s1;
-            out[nt] = t;
-        }
-        nt++;
-    };
-    for (int c = 0; c < mt; c++) {
-        long long cs = offset[(long long)(ig + c) * g.P];
-        long long ce = offset[(long long)(ig + c + 1) * g.P];
-        long long cnt = ce - cs;
-        if (cnt == 0) continue;
-        if (cur > 0 && (cur + cnt > tile_max || c - c0 + 1 > max_span)) {
-            emit(c0, c - 1 < c0 ? c0 : c - 1, tstart, cs);
-            cur = 0;
-            tstart = cs;
-            c0 = c;
-        }
-        if (cur == 0) { tstart = cs; c0 = c; }
-        cur += cnt;
-        while (cur > tile_max) {
-            emit(c0, c, tstart, tstart + tile_max);
-            tstart += tile_max;
-            cur -= tile_max;
-            c0 = c;
-        }
-    }
-    if (cur > 0) emit(c0, mt - 1, tstart, tstart + cur);
-    return nt;
-}
-
 // Tiles.  max_span[i] = the widest label-cell span of ring i whose window
 // (all planes, radial band, label windows) fits the shared-memory capacity;
 // a geometry constant, computed once at init by a 32-ary search (one
