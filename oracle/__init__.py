@@ -83,7 +83,7 @@ def lib():
             "orc_push": (C.c_int64, [P, C.c_int32, C.c_int64, C.POINTER(d), C.POINTER(d), d,
                                      C.c_int32, C.c_int32, d]),
             "orc_shift_dest": (None, [P, C.c_int64, d, C.c_int32, i32]),
-            "orc_bin_key": (None, [P, C.c_int64, d, d, d, C.c_int32, C.c_int32, i64]),
+            "orc_bin_key": (None, [P, C.c_int64, d, d, d, d, C.c_int32, C.c_int32, C.c_int32, i64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -240,11 +240,14 @@ def shift_dest(p: Params, zeta: np.ndarray, P: int) -> np.ndarray:
     return out
 
 
-def bin_key(p: Params, parts: dict, k0: int = 0, P: int | None = None) -> np.ndarray:
+def bin_key(p: Params, parts: dict, k0: int = 0, P: int | None = None, nmu: int = 1) -> np.ndarray:
+    """H-4 bin key; nmu > 1 refines it by magnetic-moment quantile sub-bins."""
     P = p.mzetamax if P is None else P
     a = [_f64(parts[k]) for k in ("psi", "theta", "zeta")]
+    mu = _f64(parts["mu"]) if nmu > 1 else np.zeros(len(a[0]))
     out = np.zeros(len(a[0]), np.int64)
-    lib().orc_bin_key(C.byref(p), len(a[0]), *[_d(x) for x in a], k0, P, out.ctypes.data_as(C.POINTER(C.c_int64)))
+    lib().orc_bin_key(C.byref(p), len(a[0]), *[_d(x) for x in a], _d(mu), k0, P, nmu,
+                      out.ctypes.data_as(C.POINTER(C.c_int64)))
     return out
 
 

@@ -728,9 +728,12 @@ void orc_shift_dest(const orc_params* p, int64_t n, const double* zeta, int32_t 
 /* H-4 (reading; "sorting particles based on their cell
  * association"): cell key = (igrid_i + c) * P + k where i is the gyrocenter's
  * radial cell (Q-4 formula), c = floor(frac((theta - zeta qtinv_i)/2 pi) *
- * mtheta_i) its label cell on ring i and k its local plane interval. */
+ * mtheta_i) its label cell on ring i and k its local plane interval; refined
+ * by nmu magnetic-moment sub-bins (DESIGN H-4): key * nmu + b, b = number of
+ * thresholds -ln(1 - q/nmu), q = 1..nmu-1, that mu reaches.  nmu = 1: the
+ * plain cell key (mu may be NULL). */
 void orc_bin_key(const orc_params* p, int64_t n, const double* psi, const double* theta,
-                 const double* zeta, int32_t k0, int32_t P, int64_t* key) {
+                 const double* zeta, const double* mu, int32_t k0, int32_t P, int32_t nmu, int64_t* key) {
     orc_geom g;
     geom_build(p, &g);
     double dr = orc_dr(p);
@@ -752,7 +755,10 @@ void orc_bin_key(const orc_params* p, int64_t n, const double* psi, const double
         int32_t k = kg - k0;
         if (k < 0) k = 0;
         if (k > P - 1) k = P - 1;
-        key[ip] = (g.igrid[i] + c) * (int64_t)P + k;
+        int32_t b = 0;
+        for (int32_t q = 1; q < nmu; q++)
+            if (mu[ip] >= -log(1.0 - (double)q / nmu)) b++;
+        key[ip] = ((g.igrid[i] + c) * (int64_t)P + k) * nmu + b;
     }
     geom_free(&g);
 }

@@ -33,7 +33,7 @@ class GtcpError(RuntimeError):
 class Params(C.Structure):
     _fields_ = [
         ("mpsi", C.c_int32), ("mthetamax", C.c_int32), ("mzetamax", C.c_int32), ("micell", C.c_int32),
-        ("ntoroidal", C.c_int32), ("npartdom", C.c_int32), ("nradial", C.c_int32), ("reserved0", C.c_int32),
+        ("ntoroidal", C.c_int32), ("npartdom", C.c_int32), ("nradial", C.c_int32), ("bin_mu", C.c_int32),
         ("precision", C.c_int32), ("bin_every", C.c_int32),
         ("poisson_iters", C.c_int32), ("paranl", C.c_int32), ("drifts", C.c_int32), ("track_ids", C.c_int32),
         ("a0", C.c_double), ("a1", C.c_double), ("R0", C.c_double), ("omega0", C.c_double),

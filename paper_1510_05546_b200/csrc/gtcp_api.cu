@@ -227,7 +227,7 @@ extern "C" gtcp_status gtcp_default_params(char size, gtcp_params* out) {
     memset(&p, 0, sizeof(p));
     p.mpsi = mpsi; p.mthetamax = mth; p.mzetamax = mze; p.micell = micell;
     p.ntoroidal = 1; p.npartdom = 1; p.nradial = 1;
-    p.precision = 64; p.bin_every = 2; p.poisson_iters = 20; p.paranl = 1; p.drifts = 1; p.track_ids = 0;
+    p.precision = 64; p.bin_every = 2; p.bin_mu = 4; p.poisson_iters = 20; p.paranl = 1; p.drifts = 1; p.track_ids = 0;
     p.a0 = 0.1; p.a1 = 0.9; p.R0 = 2.78; p.omega0 = 125.0 * mpsi / 90.0;
     p.q0 = 0.854; p.q2 = 2.184; p.rln = 2.2; p.rlt = 6.9; p.tau = 1.0; p.dt = 0.06;
     p.jacobi_omega = 1.0; p.w_init_amp = 1e-3; p.vcut = 5.0; p.capacity_factor = 1.0;
@@ -276,6 +276,7 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     if (p->mpsi < 2 || p->mthetamax < 4 || p->mzetamax < 2 || p->micell < 0) return GTCP_EINVAL;
     const int nrad = p->nradial < 1 ? 1 : p->nradial;
     if (p->ntoroidal < 1 || p->npartdom < 1 || nrad > 8) return GTCP_EINVAL;
+    if (p->bin_mu < 1 || p->bin_mu > 8) return GTCP_EINVAL;
     if (p->mzetamax % p->ntoroidal != 0 || p->ntoroidal * nrad * p->npartdom != nranks) return GTCP_EINVARIANT;
     if (p->mzetamax / p->ntoroidal < 2) return GTCP_EINVARIANT;
     if (nranks > 1 && !nccl_id) return GTCP_EINVAL;
@@ -329,6 +330,8 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     g.rln = p->rln; g.rlt = p->rlt; g.tau = p->tau; g.dt = p->dt;
     g.cz = p->mzetamax / GTCP_TWO_PI;
     g.psi_lo = 0.5 * g.a0 * g.a0 * (1.0 + 1e-12);
+    g.nmu = p->bin_mu;  // H-4 mu sub-bins: thresholds at the Exp(1) quantiles b / nmu
+    for (int b = 1; b < g.nmu; b++) g.mu_thr[b - 1] = -std::log(1.0 - (double)b / g.nmu);
     g.psi_hi = 0.5 * g.a1 * g.a1 * (1.0 - 1e-12);
     g.dzeta = GTCP_TWO_PI / p->mzetamax;
     g.rhoG = std::sqrt(2.0) / p->omega0;
@@ -370,7 +373,7 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
         CU(dalloc(&c->id_scratch, c->cap));
     }
     // binning
-    c->nkeys = (long long)mg * P;
+    c->nkeys = (long long)mg * P * c->geo.nmu;
     CU(dalloc(&c->key, c->cap));
     CU(dalloc(&c->rankbuf, c->cap));
     CU(dalloc(&c->count, c->nkeys + 1));

@@ -1269,7 +1269,7 @@ void launch_wmax(const double* w, long long n, DevCounters* dc, cudaStream_t st)
 // bin (H-4): key = (igrid_i + c) * P + k, same operation sequence as the
 // oracle so the key is bit-exact; counting sort by key.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned bin_key(const Geo& g, double psi, double theta, double zeta) {
+__device__ __forceinline__ unsigned bin_key(const Geo& g, double psi, double theta, double zeta, double mu) {
     double r = sqrt(__dmul_rn(2.0, psi));
     double x = __ddiv_rn(__dsub_rn(r, g.a0), g.dr);
     int i = (int)floor(x);
@@ -1283,7 +1283,9 @@ __device__ __forceinline__ unsigned bin_key(const Geo& g, double psi, double the
     double wz1;
     int k = plane_of(g, zeta, &wz1) - g.k0;
     k = min(max(k, 0), g.P - 1);
-    return (unsigned)((__ldg(g.igrid + i) + c) * g.P + k);
+    int mb = 0;  // magnetic-moment bin (constant per marker): gyroradius-coherent warps
+    for (int b = 0; b < g.nmu - 1; b++) mb += (mu >= g.mu_thr[b]);
+    return (unsigned)(((__ldg(g.igrid + i) + c) * g.P + k) * g.nmu + mb);
 }
 
 template <class R>
@@ -1295,7 +1297,7 @@ __global__ void k_bin_keys(Geo g, PSet s, long long n, unsigned* __restrict__ ke
     for (long long p0 = (long long)blockIdx.x * blockDim.x; p0 < n; p0 += (long long)gridDim.x * blockDim.x) {
         const long long p = p0 + threadIdx.x;
         const bool act = p < n;
-        unsigned kk = act ? bin_key(g, ldp<R>(s.x[0], p), ldp<R>(s.x[1], p), ldp<R>(s.x[2], p)) : 0xffffffffu;
+        unsigned kk = act ? bin_key(g, ldp<R>(s.x[0], p), ldp<R>(s.x[1], p), ldp<R>(s.x[2], p), ldp<R>(s.mu, p)) : 0xffffffffu;
         const unsigned peers = __match_any_sync(0xffffffffu, kk);
         const int leader = __ffs(peers) - 1;
         unsigned base = 0;
@@ -1567,7 +1569,8 @@ __device__ int ring_tiles_warp(const Geo& g, int i, const unsigned* __restrict__
     const int lane = threadIdx.x & 31;
     const int mt = __ldg(g.mtheta + i), ig = __ldg(g.igrid + i);
     int nt = 0, c0 = 0;
-    long long cur = 0, tstart = offset[(long long)ig * g.P];
+    const long long ks = (long long)g.P * g.nmu;  // keys per cell
+    long long cur = 0, tstart = offset[(long long)ig * ks];
     auto emit = [&](int a, int b, long long s0, long long s1) {
         if (s1 <= s0) return;
         if (out && nt < max_out) {
@@ -1581,8 +1584,8 @@ __device__ int ring_tiles_warp(const Geo& g, int i, const unsigned* __restrict__
         const int cl = cb + lane;
         unsigned cs_l = 0, ce_l = 0;
         if (cl < mt) {
-            cs_l = offset[(long long)(ig + cl) * g.P];
-            ce_l = offset[(long long)(ig + cl + 1) * g.P];
+            cs_l = offset[(long long)(ig + cl) * ks];
+            ce_l = offset[(long long)(ig + cl + 1) * ks];
         }
         const int nq = min(32, mt - cb);
         for (int q = 0; q < nq; q++) {

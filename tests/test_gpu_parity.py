@@ -195,7 +195,7 @@ def test_bin_keys_sorted_and_permutation(G, orc, T):
     ctx = ctx_for(G, "T")
     ctx.set_particles(parts)  # bins
     got = ctx.get_particles()
-    keys = orc.bin_key(p, got)
+    keys = orc.bin_key(p, got, nmu=G.gtcp_default_params("T").bin_mu)  # H-4 incl. mu sub-bins
     assert np.all(np.diff(keys) >= 0)
     order = np.argsort(got["id"])
     assert np.array_equal(got["id"][order], parts["id"])

@@ -57,3 +57,27 @@ def test_bin_key_cell_centres(orc):
     parts = dict(psi=a[:, 0], theta=a[:, 1], zeta=a[:, 2])
     key = orc.bin_key(p, parts)
     assert np.array_equal(key, a[:, 3].astype(np.int64))
+
+
+def test_bin_key_mu_subbins_refine_the_cell_key(orc):
+    """H-4 with nmu magnetic-moment sub-bins: key // nmu is the plain cell key,
+    the sub-bin is monotone in mu, and for mu ~ Exp(1) (the loader's
+    v_perp^2 / 2B at B = 1) each of the nmu quantile bins holds 1/nmu of the
+    markers."""
+    cfg = synth.config("T")
+    p = orc.make_params(cfg)
+    parts = synth.load_particles(cfg, 20000, seed=5)
+    rng = np.random.default_rng(11)
+    parts["mu"] = rng.exponential(1.0, len(parts["psi"]))
+    k1 = orc.bin_key(p, parts)
+    for nmu in (2, 4, 8):
+        kn = orc.bin_key(p, parts, nmu=nmu)
+        assert np.array_equal(kn // nmu, k1)
+        b = kn % nmu
+        frac = np.bincount(b, minlength=nmu) / len(b)
+        assert np.all(np.abs(frac - 1.0 / nmu) < 0.02), frac
+        order = np.argsort(parts["mu"])
+        same = {k: np.repeat(parts[k][:1], len(order)) for k in ("psi", "theta", "zeta")}
+        same["mu"] = parts["mu"][order]
+        bs = orc.bin_key(p, same, nmu=nmu) % nmu
+        assert np.all(np.diff(bs) >= 0)
