@@ -78,7 +78,7 @@ typedef struct {
      * rank = (toroidal * nradial + radial) * npartdom + particle replica.
      * Radial domains: equal-area windows snapped to rings (G-6). */
     int32_t ntoroidal, npartdom, nradial;
-    int32_t bin_mu;         /* magnetic-moment sub-bins of the bin key, 1..8 (H-4): markers of
+    int32_t bin_mu;         /* magnetic-moment sub-bins of the bin key, 1..16 (H-4): markers of
                              * one (cell, plane) are further ordered by their mu quantile
                              * (Exp(1) quantiles) so that a warp shares gyroradii; 4 */
     int32_t precision;      /* 64: fp64 state; 32: fp32 state (class D), fp64 arithmetic */

@@ -276,7 +276,7 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     if (p->mpsi < 2 || p->mthetamax < 4 || p->mzetamax < 2 || p->micell < 0) return GTCP_EINVAL;
     const int nrad = p->nradial < 1 ? 1 : p->nradial;
     if (p->ntoroidal < 1 || p->npartdom < 1 || nrad > 8) return GTCP_EINVAL;
-    if (p->bin_mu < 1 || p->bin_mu > 8) return GTCP_EINVAL;
+    if (p->bin_mu < 1 || p->bin_mu > 16) return GTCP_EINVAL;
     if (p->mzetamax % p->ntoroidal != 0 || p->ntoroidal * nrad * p->npartdom != nranks) return GTCP_EINVARIANT;
     if (p->mzetamax / p->ntoroidal < 2) return GTCP_EINVARIANT;
     if (nranks > 1 && !nccl_id) return GTCP_EINVAL;

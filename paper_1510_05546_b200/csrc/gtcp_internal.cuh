@@ -16,7 +16,7 @@
 struct Geo {
     int mpsi, mzetamax, P, k0;     // rings, global planes, local planes, first local plane
     int nmu;                       // magnetic-moment bins in the bin key (1 = off)
-    double mu_thr[7];              // their thresholds (Exp(1) quantiles of mu)
+    double mu_thr[15];             // their thresholds (Exp(1) quantiles of mu)
     int ntor, rank_t;              // toroidal domains, this rank's toroidal index
     int nrad, rank_r;              // radial domains, this rank's radial index
     double rbound[9];              // radial domain boundaries r(b_0 = ring 0) .. r(b_nrad = ring mpsi)
