@@ -32,6 +32,7 @@ struct gtcp_ctx_s {
     int mgrid = 0, P = 0, k0 = 0;
     int *d_mtheta = nullptr, *d_igrid = nullptr, *d_itran = nullptr;
     unsigned short* d_node_ring = nullptr;
+    PoisRing* d_pois = nullptr;  // F-1 per-ring constants (Poisson operator)
     double* d_qtinv = nullptr;
     Geo geo;
     // particles
@@ -343,6 +344,37 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     for (int b = 0; b <= nrad; b++) g.rbound[b] = p->a0 + c->rad_ring[b] * g.dr;
     g.mtheta = c->d_mtheta; g.igrid = c->d_igrid; g.itran = c->d_itran; g.qtinv = c->d_qtinv;
     g.node_ring = c->d_node_ring;
+    {
+        // F-1 per-ring constants, same point definitions as the oracle's operator:
+        // theta-points (r_i, theta +- rhoG/r_i), radial points (r_i +- rhoG, theta)
+        std::vector<PoisRing> pr(M + 1);
+        for (int i = 0; i <= M; i++) {
+            PoisRing& R = pr[i];
+            const double r = g.a0 + i * g.dr;
+            const int mt = c->mtheta[i];
+            R.mt = mt;
+            R.ig = c->igrid[i];
+            R.dlab = g.rhoG / r * mt / GTCP_TWO_PI;
+            for (int sg = 0; sg < 2; sg++) {
+                double rs = sg == 0 ? r + g.rhoG : r - g.rhoG;
+                rs = std::min(std::max(rs, g.a0), g.a1);
+                const double x = (rs - g.a0) * g.inv_dr;
+                const int m = std::min(std::max((int)std::floor(x), 0), M - 1);
+                R.m[sg] = m;
+                R.wp[sg] = x - m;
+                for (int q = 0; q < 2; q++) {
+                    const int mm = m + q, t = 2 * sg + q;
+                    R.mtm[t] = c->mtheta[mm];
+                    R.igm[t] = c->igrid[mm];
+                    R.ratio[t] = (double)c->mtheta[mm] / mt;
+                    R.cz[t] = (c->qtinv[i] - c->qtinv[mm]) * c->mtheta[mm] / GTCP_TWO_PI;
+                    R.inv_mt[t] = 1.0 / c->mtheta[mm];
+                }
+            }
+        }
+        CU(dalloc(&c->d_pois, M + 1));
+        CU(cudaMemcpy(c->d_pois, pr.data(), sizeof(PoisRing) * (M + 1), cudaMemcpyHostToDevice));
+    }
     // particle capacity: the loaded count plus headroom for shift imbalance
     long long per_plane = (long long)p->micell * (mg - M);
     long long n_load = per_plane * P / p->npartdom;
@@ -510,7 +542,7 @@ extern "C" void gtcp_destroy(gtcp_ctx c) {
     F(c->key); F(c->rankbuf); F(c->count); F(c->offset); F(c->scan_tmp); F(c->tiles); F(c->tile_span);
     F(c->fx); F(c->rhoH); F(c->dnH); F(c->tmpH); F(c->phiH); F(c->rhs); F(c->jphi); F(c->g1); F(c->g2);
     F(c->gfield); F(c->nm); F(c->ringsum); F(c->phi00); F(c->halo_buf); F(c->fx_recv); F(c->dc); F(c->d_scalar); F(c->d_partial);
-    F(c->d_mtheta); F(c->d_igrid); F(c->d_itran); F(c->d_qtinv); F(c->d_node_ring);
+    F(c->d_mtheta); F(c->d_igrid); F(c->d_itran); F(c->d_qtinv); F(c->d_node_ring); F(c->d_pois);
     for (int d = 0; d < 12; d++) { F(c->sendL[d]); F(c->sendR[d]); F(c->recvL[d]); F(c->recvR[d]); }
     F(c->sidL); F(c->sidR); F(c->ridL); F(c->ridR); F(c->cls); F(c->bcount); F(c->holes); F(c->fills); F(c->midx); F(c->d_nkeep);
     F(c->d_counts);
@@ -735,8 +767,8 @@ extern "C" gtcp_status gtcp_poisson_smooth(gtcp_ctx c) {
     if (c->prm.ntoroidal > 1) NC(ncclAllReduce(c->ringsum, c->ringsum, g.mpsi + 1, ncclDouble, ncclSum, c->tor, c->st));
     launch_jacobi_init(g, c->dnH, c->ringsum, c->rhs, c->jphi, c->st);
     for (int it = 0; it < c->prm.poisson_iters; it++) {
-        launch_gyro(g, c->jphi, c->g1, c->st);
-        launch_gyro_jacobi(g, c->g1, c->rhs, c->jphi, c->prm.jacobi_omega, c->st);
+        launch_gyro(g, c->d_pois, c->jphi, c->g1, c->st);
+        launch_gyro_jacobi(g, c->d_pois, c->g1, c->rhs, c->jphi, c->prm.jacobi_omega, c->st);
     }
     launch_zonal(g, c->ringsum, c->phi00, c->st);
     launch_add_zonal2(g, c->phi00, c->jphi, c->phiH, c->st);

@@ -35,24 +35,6 @@ __device__ __forceinline__ double ring_interp(const Geo& g, const double* pl, in
     return (1.0 - wt1) * ring[j] + wt1 * ring[j1];
 }
 
-__device__ __forceinline__ double plane_interp(const Geo& g, const double* pl, double r, double th, double zk) {
-    r = fmin(fmax(r, g.a0), g.a1);
-    double x = (r - g.a0) * g.inv_dr;
-    int i = min(max((int)floor(x), 0), g.mpsi - 1);
-    double wp1 = x - i;
-    return (1.0 - wp1) * ring_interp(g, pl, i, th, zk) + wp1 * ring_interp(g, pl, i + 1, th, zk);
-}
-
-// F-1 four-point gyro-average at node (ring i, label j) of plane array pl.
-// The two theta-points sit on ring i itself (r = r_i: the radial weight of
-// ring i is 1 up to rounding), so they interpolate on ring i only.
-__device__ __forceinline__ double gyro_value(const Geo& g, const double* pl, int i, int j, int mt, double zk) {
-    const double r = g.a0 + i * g.dr;
-    const double th = j * (GTCP_TWO_PI / mt) + zk * __ldg(g.qtinv + i);
-    const double dth = g.rhoG / r;
-    return 0.25 * (plane_interp(g, pl, r + g.rhoG, th, zk) + ring_interp(g, pl, i, th + dth, zk) +
-                   plane_interp(g, pl, r - g.rhoG, th, zk) + ring_interp(g, pl, i, th - dth, zk));
-}
 
 // copy canonical j=0 into the duplicate j=mtheta on `planes` planes (ncomp interleaved)
 __global__ void k_fill_dup(Geo g, double* f, int planes, int ncomp) {
@@ -251,67 +233,90 @@ void launch_jacobi_init(const Geo& g, const double* dn, const double* ringsum, d
     g_launches++;
 }
 
-// F-1 four-point gyro-average on every owned plane (plain arrays)
-__global__ void k_gyro(Geo g, const double* __restrict__ in, double* __restrict__ out) {
-    long long total = (long long)g.P * g.mgrid;
-    GRID_LOOP(e, total) {
-        int k = (int)(e / g.mgrid), node = (int)(e % g.mgrid);
-        int i = ring_of(g, node);
-        int mt = __ldg(g.mtheta + i);
-        int j = node - __ldg(g.igrid + i);
-        if (j == mt) j = 0;
-        const double* pl = in + (long long)k * g.mgrid;
-        out[e] = gyro_value(g, pl, i, j, mt, (double)(g.k0 + k) * g.dzeta);
-    }
+// value of a ring at fractional label s in [0, mt): linear in the label, periodic
+__device__ __forceinline__ double lerp_ring(const double* ring, int mt, double s) {
+    const int j0 = min((int)floor(s), mt - 1);
+    const double w = s - j0;
+    const int j1 = (j0 + 1 == mt) ? 0 : j0 + 1;
+    return (1.0 - w) * ring[j0] + w * ring[j1];
 }
 
-void launch_gyro(const Geo& g, const double* in, double* out, cudaStream_t st) {
-    k_gyro<<<blocks_for((long long)g.P * g.mgrid), 256, 0, st>>>(g, in, out);
+// F-1 four-point gyro-average at node (ring i, label j) of plane pl at plane
+// angle zk: points (r_i +- rhoG, theta) interpolated between their bounding
+// rings, (r_i, theta +- rhoG / r_i) on ring i (r = r_i: radial weight 1), each
+// label from the per-ring constants with one fma.
+__device__ __forceinline__ double gyro_value_tab(const PoisRing* __restrict__ R, const double* pl, int j,
+                                                 double zk) {
+    const int mt = R->mt;
+    const double* ring = pl + R->ig;
+    double s = (double)j + R->dlab;
+    if (s >= mt) s -= mt;
+    double v = lerp_ring(ring, mt, s);
+    s = (double)j - R->dlab;
+    if (s < 0.0) s += mt;
+    v += lerp_ring(ring, mt, s);
+#pragma unroll
+    for (int sg = 0; sg < 2; sg++) {
+        const double wp = R->wp[sg];
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+            const int t = 2 * sg + q;
+            const int mtm = R->mtm[t];
+            double y = fma((double)j, R->ratio[t], zk * R->cz[t]) * R->inv_mt[t];
+            y = (y - floor(y)) * mtm;
+            acc += (q ? wp : 1.0 - wp) * lerp_ring(pl + R->igm[t], mtm, y);
+        }
+        v += acc;
+    }
+    return 0.25 * v;
+}
+
+// F-1 on every owned plane (plain arrays); grid (nodes, planes)
+__global__ void k_gyro(Geo g, const PoisRing* __restrict__ pr, const double* __restrict__ in,
+                       double* __restrict__ out) {
+    const int k = blockIdx.y;
+    const int node = blockIdx.x * blockDim.x + threadIdx.x;
+    if (node >= g.mgrid) return;
+    const long long e = (long long)k * g.mgrid + node;
+    const int i = ring_of(g, node);
+    const PoisRing* R = pr + i;
+    int j = node - R->ig;
+    if (j == R->mt) j = 0;
+    out[e] = gyro_value_tab(R, in + (long long)k * g.mgrid, j, (double)(g.k0 + k) * g.dzeta);
+}
+
+static dim3 grid_nodes_planes(const Geo& g) { return dim3((unsigned)((g.mgrid + 255) / 256), (unsigned)g.P); }
+
+void launch_gyro(const Geo& g, const PoisRing* pr, const double* in, double* out, cudaStream_t st) {
+    k_gyro<<<grid_nodes_planes(g), 256, 0, st>>>(g, pr, in, out);
     g_launches++;
-}
-
-__global__ void k_jacobi_update(Geo g, const double* __restrict__ rhs, const double* __restrict__ g2,
-                                double* __restrict__ phi, double omega) {
-    long long total = (long long)g.P * g.mgrid;
-    const double c0 = 1.0 + 1.0 / g.tau;
-    GRID_LOOP(e, total) {
-        int node = (int)(e % g.mgrid);
-        int i = ring_of(g, node);
-        double v = (1.0 - omega) * phi[e] + omega * (rhs[e] + g2[e]) / c0;
-        phi[e] = (i == 0 || i == g.mpsi) ? 0.0 : v;
-    }
 }
 
 // second G application fused with the Jacobi update (F-2):
 // phi <- (1-omega) phi + omega (rhs + G(g1)) / (1 + 1/tau), phi = 0 on rings 0, mpsi
-__global__ void k_gyro_jacobi(Geo g, const double* __restrict__ g1, const double* __restrict__ rhs,
-                              double* __restrict__ phi, double omega) {
-    long long total = (long long)g.P * g.mgrid;
+__global__ void k_gyro_jacobi(Geo g, const PoisRing* __restrict__ pr, const double* __restrict__ g1,
+                              const double* __restrict__ rhs, double* __restrict__ phi, double omega) {
+    const int k = blockIdx.y;
+    const int node = blockIdx.x * blockDim.x + threadIdx.x;
+    if (node >= g.mgrid) return;
+    const long long e = (long long)k * g.mgrid + node;
+    const int i = ring_of(g, node);
+    if (i == 0 || i == g.mpsi) { phi[e] = 0.0; return; }
     const double c0 = 1.0 + 1.0 / g.tau;
-    GRID_LOOP(e, total) {
-        int k = (int)(e / g.mgrid), node = (int)(e % g.mgrid);
-        int i = ring_of(g, node);
-        if (i == 0 || i == g.mpsi) { phi[e] = 0.0; continue; }
-        int mt = __ldg(g.mtheta + i);
-        int j = node - __ldg(g.igrid + i);
-        if (j == mt) j = 0;
-        const double* pl = g1 + (long long)k * g.mgrid;
-        const double v = gyro_value(g, pl, i, j, mt, (double)(g.k0 + k) * g.dzeta);
-        phi[e] = (1.0 - omega) * phi[e] + omega * (rhs[e] + v) / c0;
-    }
+    const PoisRing* R = pr + i;
+    int j = node - R->ig;
+    if (j == R->mt) j = 0;
+    const double v = gyro_value_tab(R, g1 + (long long)k * g.mgrid, j, (double)(g.k0 + k) * g.dzeta);
+    phi[e] = (1.0 - omega) * phi[e] + omega * (rhs[e] + v) / c0;
 }
 
-void launch_gyro_jacobi(const Geo& g, const double* g1, const double* rhs, double* phi, double omega,
-                        cudaStream_t st) {
-    k_gyro_jacobi<<<blocks_for((long long)g.P * g.mgrid), 256, 0, st>>>(g, g1, rhs, phi, omega);
+void launch_gyro_jacobi(const Geo& g, const PoisRing* pr, const double* g1, const double* rhs, double* phi,
+                        double omega, cudaStream_t st) {
+    k_gyro_jacobi<<<grid_nodes_planes(g), 256, 0, st>>>(g, pr, g1, rhs, phi, omega);
     g_launches++;
 }
 
-void launch_jacobi_update(const Geo& g, const double* rhs, const double* g2, double* phi, double omega,
-                          cudaStream_t st) {
-    k_jacobi_update<<<blocks_for((long long)g.P * g.mgrid), 256, 0, st>>>(g, rhs, g2, phi, omega);
-    g_launches++;
-}
 
 // F-3 zonal flow: -rho_i^2 (1/r)(r phi00')' = <dn>, Dirichlet ends, Thomas algorithm.
 // ringsum holds the global ring sums of dn (mean = sum / (mzetamax * mtheta)).

@@ -38,6 +38,19 @@ struct Geo {
 
 // One charge tile: particles [start, end) of the cell-sorted store whose
 // gyrocentre cell (ring, label) lay in ring `ring`, cells [c0, c1] at bin time.
+// Per-ring constants of the F-1 gyro-average on the grid (Poisson operator),
+// host-computed once: the theta-points' label offset on the node's own ring,
+// and for the radial points r_i +- rhoG (s = 0, 1) their floor ring m_s, upper
+// weight and, for rings m_s + q, the label map j -> j * ratio + zk * cz.
+struct PoisRing {
+    double dlab;
+    double wp[2];
+    double ratio[4], cz[4], inv_mt[4];
+    int m[2];
+    int mt, ig;
+    int mtm[4], igm[4];
+};
+
 struct Tile {
     int ring, c0, c1, pad;
     long long start, end;
@@ -120,11 +133,9 @@ void launch_smooth_par(const Geo& g, const double* in, double* out, cudaStream_t
 void launch_ring_sum(const Geo& g, const double* f, double* ringsum, cudaStream_t st);
 void launch_jacobi_init(const Geo& g, const double* dn, const double* ringsum, double* rhs, double* phi,
                         cudaStream_t st);
-void launch_gyro(const Geo& g, const double* in, double* out, cudaStream_t st);
-void launch_gyro_jacobi(const Geo& g, const double* g1, const double* rhs, double* phi, double omega,
-                        cudaStream_t st);
-void launch_jacobi_update(const Geo& g, const double* rhs, const double* g2, double* phi, double omega,
-                          cudaStream_t st);
+void launch_gyro(const Geo& g, const PoisRing* pr, const double* in, double* out, cudaStream_t st);
+void launch_gyro_jacobi(const Geo& g, const PoisRing* pr, const double* g1, const double* rhs, double* phi,
+                        double omega, cudaStream_t st);
 void launch_zonal(const Geo& g, const double* ringsum, double* phi00, cudaStream_t st);
 void launch_add_zonal2(const Geo& g, const double* phi00, const double* phi, double* phiH, cudaStream_t st);
 void launch_field(const Geo& g, const double* phi, double* gfield, cudaStream_t st);
