@@ -43,6 +43,14 @@ __device__ __forceinline__ double cos_theta(double theta) { return cospi(theta *
 __device__ __forceinline__ void sincos_theta(double theta, double* s, double* c) { sincospi(theta * kInvPi, s, c); }
 static constexpr int kMaxRings = 16;   // radial band of one tile window
 static constexpr int kDepositThreads = 256;
+// plane stride of a tile window = kPlanePad (mod 32) words: picked with the
+// bank-conflict model tools/bank_sim.py (mean 4.1 wavefronts per ATOMS over
+// A and B/2, B/4, B/8 windows vs 4.7 for 16 mod 32, whose stride aligns with
+// the ~16-column rings of the B/4 windows)
+#ifndef GTCP_PLANE_PAD
+#define GTCP_PLANE_PAD 4
+#endif
+static constexpr int kPlanePad = GTCP_PLANE_PAD;
 
 // round-to-nearest-even integer of a*b for |a*b| < 2^51 (1.5*2^52 magic
 // constant, one fused rounding).  Explicit intrinsics: every kernel computes
@@ -257,7 +265,7 @@ __device__ __forceinline__ int win_nodes(const Geo& g, int i, int c0, int c1, do
     int m_lo = max(0, i - h), m_hi = min(g.mpsi, i + 1 + h);
     int S = 0;
     for (int m = m_lo; m <= m_hi; m++) S += win_width(g, i, c0, c1, m, rho_cut) + 1;  // + trash column
-    S += (16 - (S & 31) + 32) & 31;  // the plane-stride padding of k_deposit_tiled
+    S += (kPlanePad - (S & 31) + 32) & 31;  // the plane-stride padding of k_deposit_tiled
     return S * (g.P + 1);
 }
 
@@ -349,7 +357,7 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
             for (int q = 0; q < nr; q++) S += T.WO[q].x + 1;  // column W of each ring: its trash column
             // pad the plane stride to 16 (mod 32) words: the lane bit that picks
             // plane k or k+1 then always flips the shared-memory bank half
-            S += (16 - (S & 31) + 32) & 31;
+            S += (kPlanePad - (S & 31) + 32) & 31;
             const bool fits = S * P1 <= cap_nodes;  // else: everything via L2
             __syncthreads();
             if (threadIdx.x == 0) {

@@ -17,6 +17,7 @@ ap.add_argument("--bin-every", type=int, default=2)
 ap.add_argument("--tag", default="")
 ap.add_argument("--micell", type=int, default=None)
 ap.add_argument("--bin-mu", type=int, default=None)
+ap.add_argument("--mzetamax", type=int, default=None)
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -27,6 +28,8 @@ torch.cuda.set_device(0)
 over = {"micell": a.micell} if a.micell else {}
 if a.bin_mu:
     over["bin_mu"] = a.bin_mu
+if a.mzetamax:
+    over["mzetamax"] = a.mzetamax
 stream = torch.cuda.Stream()
 ctx = G.Context(G.gtcp_default_params(a.size, bin_every=a.bin_every, **over), stream=stream.cuda_stream)
 ctx.set_charge_mode(a.charge_mode)
