@@ -56,6 +56,16 @@ def build(size, mzetamax, ring_frac, tile_max, nmu, seed, layout):
     key = ((ig[i] + C) * P + K) * nmu + mb
     order = np.lexsort((rng.random(n), key))
     r, zeta, theta, invB, mu, K = r[order], zeta[order], theta[order], invB[order], mu[order], K[order]
+    # streaming since the bin: `age` stages of parallel motion (v_par ~ N(0, 1),
+    # zeta advances v_par B / R0 per unit time, theta follows the field line)
+    age = layout.get("age", 0.0)
+    if age:
+        vpar = rng.standard_normal(n)
+        dzeta = vpar / p.R0 * (0.5 * p.dt) * age
+        zeta = zeta + dzeta
+        theta = np.mod(theta + dzeta * qt[i], TWO_PI)
+        K = np.clip(np.floor(zeta / dz).astype(np.int64), 0, P - 1)
+        zeta = np.clip(zeta, 0, P * dz - 1e-12)
     rho = np.sqrt(2.0 * mu * invB) / om
     # window (kernel: win_halo / win_width / js)
     h = min(int(math.ceil(rho_cut / dr)) + 1, 7)
@@ -124,7 +134,10 @@ def lane_addresses(T, p0, lq, mq, kq, t, rot):
     return np.where(inband, addr, -1 - b)  # out of band: trash slot (distinct dummy)
 
 
-def wavefronts(addr):
+def wavefronts(addr, distinct=False):
+    """max over banks of the lanes (or, distinct=True, of the distinct words) on one bank"""
+    if distinct:
+        addr = np.unique(addr)
     bank = np.mod(addr, 32)
     return np.bincount(bank, minlength=32).max()
 
@@ -188,7 +201,7 @@ def lane_addresses_v(T, pidx, lq, mq, kq, t, bits):
     return np.where(inband, addr, -1 - b)
 
 
-def run_v(T, bits, mapping="contig", warps=300, seed=0):
+def run_v(T, bits, mapping="contig", warps=300, seed=0, distinct=False):
     rng = np.random.default_rng(seed)
     n = T["n"]
     nw = n // 32
@@ -210,7 +223,7 @@ def run_v(T, bits, mapping="contig", warps=300, seed=0):
                 for kq in range(2):
                     for t in range(2):
                         a = lane_addresses_v(T, pidx, lq, mq, kq, t, bits)
-                        tot += wavefronts(a)
+                        tot += wavefronts(a, distinct)
                         same += 32 - len(np.unique(a))
                         cnt += 1
     return tot / cnt, same / cnt
