@@ -311,6 +311,14 @@ __device__ __forceinline__ unsigned wrap_diff(int j, int js, int mt) {
 // (an immediate offset in the ATOMS), row table [(P+1) x kRowStride] of
 // (label window start, byte offset of the row), column -> ring bytes.
 static constexpr int kRowStride = kMaxRings + 1;
+#ifdef GTCP_DUMP_ADDR
+// debug build only: word offsets of the lo-limb ATOMS of the first 8 iterations
+// of the 8 warps of 64 tiles spread over the launch ([tile][iter][warp][32][32])
+__device__ unsigned g_addr_dump[64 * 8 * 8 * 32 * 32];
+extern "C" int gtcp_debug_addr_dump(unsigned* host) {
+    return (int)cudaMemcpyFromSymbol(host, g_addr_dump, sizeof(g_addr_dump));
+}
+#endif
 
 template <class R, int NB>
 __global__ void __launch_bounds__(kDepositThreads, NB)
@@ -511,6 +519,20 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
                         const double wzk = kq ? wzB : wzA;
                         const double ta = fx_magic(wzk, aa), tb = fx_magic(wzk, ab);
                         unsigned char* base = reinterpret_cast<unsigned char*>(slo);
+#ifdef GTCP_DUMP_ADDR  // tools/dump_addr.py: lane word offsets of sampled tiles
+                        {
+                            const int tstride = max(1, ntiles / 64), ts = t / tstride;
+                            if (t % tstride == 0 && ts < 64 && p < T.start + 2048) {
+                                const int it = (int)((p - T.start) / blockDim.x), wi = threadIdx.x >> 5;
+                                const int ins = ((lq * 2 + mq) * 2 + kq) * 2;
+                                if (it < 8) {
+                                    unsigned* d = g_addr_dump + (((size_t)(ts * 8 + it) * 8 + wi) * 32 + ins) * 32 + lane;
+                                    d[0] = oa >> 2;
+                                    d[32] = ob >> 2;
+                                }
+                            }
+                        }
+#endif
                         atomicAdd(reinterpret_cast<unsigned*>(base + oa), fx_lo(ta));
                         atomicAdd(reinterpret_cast<int*>(base + oa + 4 * kDepStride), fx_hi(ta));
                         atomicAdd(reinterpret_cast<unsigned*>(base + ob), fx_lo(tb));

@@ -1,6 +1,12 @@
-"""Debug: dump the lo-limb ATOMS word offsets of the first tiles of one
-k_deposit_tiled launch (libgtcp built with -DGTCP_DUMP_ADDR) and count the
-wavefronts per instruction (max distinct words on one bank)."""
+"""Debug: dump the lo-limb ATOMS word offsets of sampled tiles of one
+k_deposit_tiled launch and count the wavefronts per instruction (max distinct
+words on one bank).  Needs the debug build:
+  python paper_1510_05546_b200/_build.py -DGTCP_DUMP_ADDR --out=$PWD/paper_1510_05546_b200/_lib/libgtcp_dump.so
+  GTCP_LIB_PATH=$PWD/paper_1510_05546_b200/_lib/libgtcp_dump.so python tools/dump_addr.py A
+Note: ATOMS.ADD lanes on the same word serialise (each carries its own value);
+the microbenchmark's constant increments compile to ATOMS.POPC.INC, which
+merges them, so replaying these offsets (tools/microbench/replay.cu) gives
+the distinct-word count, a lower bound."""
 import ctypes
 import os
 import sys
