@@ -1,0 +1,144 @@
+"""GPU edge cases against the oracle (same tolerances as test_gpu_parity):
+empty and ragged marker counts, markers on every boundary of the domain
+(r = a0, a1; theta = 0, 2pi^-; zeta on plane boundaries and 2pi^-), markers
+whose gyro-points leave the tile window (the L2 fallback of the tiled
+deposit), zero weights."""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from test_gpu_parity import G, TOL, assert_particles_close, ctx_for, rel_err, _smooth_field  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+TWO_PI = 2 * math.pi
+
+
+def _subset(parts, idx):
+    out = {k: np.ascontiguousarray(v[idx]) for k, v in parts.items()}
+    out["id"] = np.arange(len(idx), dtype=np.uint64)
+    return out
+
+
+@pytest.fixture(scope="module")
+def Tcfg(orc):
+    cfg = synth.config("T")
+    p = orc.make_params(cfg)
+    return cfg, p, orc.geometry(p)
+
+
+def test_empty_particle_set(G, orc, Tcfg):
+    cfg, p, g = Tcfg
+    parts = _subset(synth.load_particles(cfg, 10, seed=1), np.arange(0))
+    ctx = ctx_for(G, "T")
+    ctx.set_particles(parts)
+    ctx.charge()
+    assert not np.any(ctx.get_grid(G.GRID_CHARGE))
+    ctx.set_grid(G.GRID_MARKER, np.ones(p.mpsi + 1))
+    ctx.step(1)
+    got = ctx.get_particles()
+    assert len(got["id"]) == 0
+    assert ctx.stats()["n_local"] == 0
+
+
+@pytest.mark.parametrize("n", [1, 31, 33, 257, 8193])
+def test_ragged_counts_charge_and_push(G, orc, Tcfg, n):
+    """Counts that leave a ragged warp, CTA and tile tail."""
+    cfg, p, g = Tcfg
+    parts = synth.load_particles(cfg, n, seed=100 + n, w_amp=0.1)
+    grids = []
+    for mode in (0, 1):
+        ctx = ctx_for(G, "T")
+        ctx.set_charge_mode(mode)
+        ctx.set_particles(parts)
+        ctx.charge()
+        grids.append(ctx.get_grid(G.GRID_CHARGE))
+    assert np.array_equal(grids[0], grids[1])  # tiled == direct, bitwise
+    ref = orc.charge_global(p, parts)
+    assert rel_err(grids[0], ref) <= 1e-8
+    gp = _smooth_field(orc, p, g)
+    ctx = ctx_for(G, "T")
+    ctx.set_particles(parts)
+    ctx.set_grid(G.GRID_GRADPHI, gp)
+    Xa = {k: parts[k].copy() for k in orc.ATTRS}
+    Xb = {k: parts[k].copy() for k in orc.ATTRS}
+    ctx.push(1)
+    ctx.push(2)
+    orc.push(p, 1, Xa, Xb, parts["mu"], gp)
+    orc.push(p, 2, Xa, Xb, parts["mu"], gp)
+    got = ctx.get_particles()
+    assert_particles_close({**{k: got[k] for k in orc.ATTRS}, "id": got["id"]}, {**Xa, "id": parts["id"]})
+
+
+def _boundary_markers(cfg, p, g):
+    """Every combination of boundary radii, angles and plane positions."""
+    dz = TWO_PI / p.mzetamax
+    rs = [p.a0, np.nextafter(p.a0, 1.0), 0.5 * (p.a0 + p.a1), np.nextafter(p.a1, 0.0), p.a1]
+    ths = [0.0, np.nextafter(TWO_PI, 0.0), math.pi]
+    zs = [0.0, dz, np.nextafter(dz, 0.0), np.nextafter(TWO_PI, 0.0), 0.5 * dz]
+    rows = [(0.5 * r * r, th, z) for r in rs for th in ths for z in zs]
+    n = len(rows)
+    a = np.array(rows)
+    rng = np.random.default_rng(7)
+    return {"psi": a[:, 0], "theta": a[:, 1], "zeta": a[:, 2], "rho": rng.normal(0, 1, n) / p.omega0,
+            "w": rng.uniform(-0.1, 0.1, n), "mu": rng.exponential(1.0, n), "id": np.arange(n, dtype=np.uint64)}
+
+
+def test_boundary_markers_charge_and_push(G, orc, Tcfg):
+    cfg, p, g = Tcfg
+    parts = _boundary_markers(cfg, p, g)
+    ctx = ctx_for(G, "T")
+    ctx.set_particles(parts)
+    ctx.charge()
+    got = ctx.get_grid(G.GRID_CHARGE)
+    ref = orc.charge_global(p, parts)
+    assert rel_err(got, ref) <= 1e-8
+    # charge is conserved exactly in the fixed point (A-7 clamping keeps every point on the grid)
+    assert abs(got.sum() - ref.sum()) <= 1e-9 * np.abs(parts["w"]).sum()
+    gp = _smooth_field(orc, p, g)
+    ctx.set_grid(G.GRID_GRADPHI, gp)
+    Xa = {k: parts[k].copy() for k in orc.ATTRS}
+    Xb = {k: parts[k].copy() for k in orc.ATTRS}
+    ctx.push(1)
+    ctx.push(2)
+    orc.push(p, 1, Xa, Xb, parts["mu"], gp)
+    orc.push(p, 2, Xa, Xb, parts["mu"], gp)
+    got = ctx.get_particles()
+    assert_particles_close({**{k: got[k] for k in orc.ATTRS}, "id": got["id"]}, {**Xa, "id": parts["id"]})
+    assert np.all((got["theta"] >= 0) & (got["theta"] < TWO_PI))
+    assert np.all((got["zeta"] >= 0) & (got["zeta"] < TWO_PI))
+    r = np.sqrt(2 * got["psi"])
+    assert np.all((r >= p.a0 - 1e-12) & (r <= p.a1 + 1e-12))
+
+
+def test_window_overflow_goes_through_L2(G, orc):
+    """Markers with gyroradii far beyond the tile window's 3 rho_th cut: their
+    out-of-window contributions take the deferred L2 path; the tiled result
+    still equals the direct deposit bitwise and the oracle."""
+    cfg = synth.config("A")
+    p = orc.make_params(cfg)
+    parts = synth.load_particles(cfg, 200_000, seed=9)
+    big = np.arange(0, 200_000, 50)
+    parts["mu"][big] *= 400.0  # rho x 20
+    grids = []
+    for mode in (0, 1):
+        ctx = ctx_for(G, "A")
+        ctx.set_charge_mode(mode)
+        ctx.set_particles(parts)
+        ctx.charge()
+        grids.append(ctx.get_grid(G.GRID_CHARGE))
+        if mode == 0:
+            assert ctx.stats()["charge_global_fallback"] > 0
+    assert np.array_equal(grids[0], grids[1])
+    assert rel_err(grids[0], orc.charge_global(p, parts)) <= 1e-8
+
+
+def test_zero_weights_give_zero_charge(G, Tcfg):
+    cfg, p, g = Tcfg
+    parts = synth.load_particles(cfg, 5000, seed=3)
+    parts["w"][:] = 0.0
+    ctx = ctx_for(G, "T")
+    ctx.set_particles(parts)
+    ctx.charge()
+    assert not np.any(ctx.get_grid(G.GRID_CHARGE))
