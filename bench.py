@@ -215,6 +215,10 @@ def run_gpu(args):
     ms = ev0.elapsed_time(ev1)
     tm = ctx.timings()
     launches = tm["launches"] - launches0
+    if os.environ.get("BENCH_RANK_PHASES"):  # diagnostics: per-rank phase sum vs own elapsed
+        ph = {k[:-3]: round(tm[k] / args.steps, 2) for k in tm if k.endswith("_ms")}
+        print(f"[rank {rank}] own {ms / args.steps:.2f} ms/step, phases {sum(ph.values()):.2f}: {ph}",
+              file=sys.stderr, flush=True)
     if dist:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
