@@ -213,6 +213,10 @@ def run_v(T, bits, mapping="contig", warps=300, seed=0, distinct=False):
             pidx = w * 32 + b
         elif mapping == "strided":  # lane b takes marker w + b * (n // 32)
             pidx = w + b * nw
+        elif mapping.startswith("span"):  # "spanS": lane b -> span (b % S), consecutive markers by b // S
+            S = int(mapping[4:])
+            span = n // S
+            pidx = (b % S) * span + (w % (span // (32 // S))) * (32 // S) + b // S
         else:  # "groupG": G consecutive markers per lane group, 32/G groups spread over the tile
             G = int(mapping[5:])
             ng = 32 // G
