@@ -49,7 +49,8 @@ struct gtcp_ctx_s {
     int steps_done = 0;
     // binning
     long long nkeys = 0;
-    unsigned *key = nullptr, *rankbuf = nullptr, *count = nullptr, *offset = nullptr, *scan_tmp = nullptr;
+    unsigned *key = nullptr, *rankbuf = nullptr, *inv = nullptr, *count = nullptr, *offset = nullptr,
+             *scan_tmp = nullptr;
     Tile* tiles = nullptr;
     int max_tiles = 0;
     int* tile_span = nullptr;  // per ring: widest cell span whose window fits smem; then per-ring tile counts
@@ -408,6 +409,7 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     c->nkeys = (long long)mg * P * c->geo.nmu;
     CU(dalloc(&c->key, c->cap));
     CU(dalloc(&c->rankbuf, c->cap));
+    CU(dalloc(&c->inv, c->cap));
     CU(dalloc(&c->count, c->nkeys + 1));
     CU(dalloc(&c->offset, c->nkeys + 1));
     CU(dalloc(&c->scan_tmp, (c->nkeys + 4095) / 4096 + 1));
@@ -539,7 +541,7 @@ extern "C" void gtcp_destroy(gtcp_ctx c) {
     // the live/saved/mu/scratch pointers are always a permutation of the original allocations
     for (int d = 0; d < 5; d++) { F(c->live[d]); F(c->saved[d]); }
     F(c->mu); F(c->scratch); F(c->id); F(c->id_scratch);
-    F(c->key); F(c->rankbuf); F(c->count); F(c->offset); F(c->scan_tmp); F(c->tiles); F(c->tile_span);
+    F(c->key); F(c->rankbuf); F(c->inv); F(c->count); F(c->offset); F(c->scan_tmp); F(c->tiles); F(c->tile_span);
     F(c->fx); F(c->rhoH); F(c->dnH); F(c->tmpH); F(c->phiH); F(c->rhs); F(c->jphi); F(c->g1); F(c->g2);
     F(c->gfield); F(c->nm); F(c->ringsum); F(c->phi00); F(c->halo_buf); F(c->fx_recv); F(c->dc); F(c->d_scalar); F(c->d_partial);
     F(c->d_mtheta); F(c->d_igrid); F(c->d_itran); F(c->d_qtinv); F(c->d_node_ring); F(c->d_pois);
@@ -861,13 +863,25 @@ static gtcp_status do_bin(gtcp_ctx c) {
     const Geo& g = c->geo;
     c->cls_ready = false;
     PSet s = live_set(c);
+    // GTCP_PROFILE_BIN=1: per-kernel event times of the bin on stderr (diagnostics)
+    static const bool prof = getenv("GTCP_PROFILE_BIN") != nullptr;
+    cudaEvent_t ev[8];
+    int nev = 0;
+    auto mark = [&]() {
+        if (!prof) return;
+        cudaEventCreate(&ev[nev]);
+        cudaEventRecord(ev[nev++], c->st);
+    };
+    mark();
     CU(cudaMemsetAsync(c->count, 0, (c->nkeys + 1) * sizeof(unsigned), c->st));
     launch_bin_keys(g, s, c->n, c->key, c->rankbuf, c->count, c->st);
+    mark();
     launch_scan_u32(c->count, c->offset, c->nkeys, c->scan_tmp, c->st);
-    launch_bin_dest(c->key, c->rankbuf, c->offset, c->n, c->rankbuf, c->st);
+    mark();
     // gather form: inv[dest[p]] = p once, then every array is written coalesced
     // (scatter forms measured slower: plain 40 %, smem-staged chunks 7 %)
-    launch_perm_inverse(c->rankbuf, c->n, c->key, c->st);
+    launch_bin_inverse(c->key, c->rankbuf, c->offset, c->n, c->inv, c->st);
+    mark();
     // permute live state, mu (and the saved state when mid-step) in one fused
     // gather pass into the other ping-pong set + spare arrays, then swap pointers
     std::vector<double**> arrs;
@@ -882,26 +896,39 @@ static gtcp_status do_bin(gtcp_ctx c) {
         for (int d = 0; d < 5; d++) { src[d] = c->live[d]; dst[d] = c->saved[d]; }
         src[5] = c->mu;
         dst[5] = c->scratch;
-        launch_gather_perm_multi(src, dst, 6, c->id, c->id ? c->id_scratch : nullptr, c->key, c->n, c->st);
+        launch_gather_perm_multi(src, dst, 6, c->id, c->id ? c->id_scratch : nullptr, c->inv, c->n, c->st);
         for (int d = 0; d < 5; d++) std::swap(c->live[d], c->saved[d]);
         std::swap(c->mu, c->scratch);
         if (c->id) std::swap(c->id, c->id_scratch);
     } else {
         for (double** a : arrs) {
-            launch_gather_perm_f64(*a, c->scratch, c->key, c->n, c->st);
+            launch_gather_perm_f64(*a, c->scratch, c->inv, c->n, c->st);
             double* old = *a;
             *a = c->scratch;
             c->scratch = old;
         }
         if (c->id) {
-            launch_gather_perm_u64(c->id, c->id_scratch, c->key, c->n, c->st);
+            launch_gather_perm_u64(c->id, c->id_scratch, c->inv, c->n, c->st);
             std::swap(c->id, c->id_scratch);
         }
     }
+    mark();
     launch_build_tiles(g, c->offset, c->tile_max, c->tiles, c->max_tiles, c->dc, c->tile_span,
                        c->tile_span + c->geo.mpsi, c->st);
+    mark();
     c->n_binned = c->n;
     KCHECK();
+    if (prof) {
+        cudaStreamSynchronize(c->st);
+        fprintf(stderr, "[bin r%d n=%lld] keys/scan/inverse/permute/tiles ms:", c->rank, c->n);
+        for (int i = 1; i < nev; i++) {
+            float ms;
+            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            fprintf(stderr, " %.3f", ms);
+        }
+        fprintf(stderr, "\n");
+        for (int i = 0; i < nev; i++) cudaEventDestroy(ev[i]);
+    }
     return GTCP_OK;
 }
 

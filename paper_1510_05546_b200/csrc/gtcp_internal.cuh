@@ -106,9 +106,8 @@ void launch_wmax(const double* w, long long n, DevCounters* dc, cudaStream_t st)
 void launch_bin_keys(const Geo& g, const PSet& s, long long n, unsigned* key, unsigned* rank, unsigned* count,
                      cudaStream_t st);
 void launch_scan_u32(const unsigned* in, unsigned* out, long long n, unsigned* block_tmp, cudaStream_t st);
-void launch_bin_dest(const unsigned* key, const unsigned* rank, const unsigned* offset, long long n,
-                     unsigned* dest, cudaStream_t st);
-void launch_perm_inverse(const unsigned* dest, long long n, unsigned* inv, cudaStream_t st);
+void launch_bin_inverse(const unsigned* key, const unsigned* rank, const unsigned* offset, long long n,
+                        unsigned* inv, cudaStream_t st);
 void launch_gather_perm_multi(const double* const* src, double* const* dst, int na, const unsigned long long* id_src,
                               unsigned long long* id_dst, const unsigned* inv, long long n, cudaStream_t st);
 void launch_gather_perm_f64(const double* src, double* dst, const unsigned* inv, long long n, cudaStream_t st);

@@ -1433,32 +1433,19 @@ void launch_scan_u32(const unsigned* in, unsigned* out, long long n, unsigned* b
     g_launches += 3;
 }
 
-__global__ void k_bin_dest(const unsigned* __restrict__ key, const unsigned* __restrict__ rank,
-                           const unsigned* __restrict__ offset, long long n, unsigned* __restrict__ dest) {
+// inverse permutation straight from key and rank: inv[offset[key] + rank] = p
+// (the destination of p is never stored)
+__global__ void k_bin_inverse(const unsigned* __restrict__ key, const unsigned* __restrict__ rank,
+                              const unsigned* __restrict__ offset, long long n, unsigned* __restrict__ inv) {
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
          p += (long long)gridDim.x * blockDim.x)
-        dest[p] = offset[key[p]] + rank[p];
+        inv[offset[key[p]] + rank[p]] = (unsigned)p;
 }
-
-void launch_bin_dest(const unsigned* key, const unsigned* rank, const unsigned* offset, long long n,
-                     unsigned* dest, cudaStream_t st) {
+void launch_bin_inverse(const unsigned* key, const unsigned* rank, const unsigned* offset, long long n,
+                        unsigned* inv, cudaStream_t st) {
     if (n <= 0) return;
     int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
-    k_bin_dest<<<blocks, 256, 0, st>>>(key, rank, offset, n, dest);
-    g_launches++;
-}
-
-// inverse permutation: inv[dest[p]] = p
-__global__ void k_perm_inverse(const unsigned* __restrict__ dest, long long n, unsigned* __restrict__ inv) {
-    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-         p += (long long)gridDim.x * blockDim.x)
-        inv[dest[p]] = (unsigned)p;
-}
-
-void launch_perm_inverse(const unsigned* dest, long long n, unsigned* inv, cudaStream_t st) {
-    if (n <= 0) return;
-    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
-    k_perm_inverse<<<blocks, 256, 0, st>>>(dest, n, inv);
+    k_bin_inverse<<<blocks, 256, 0, st>>>(key, rank, offset, n, inv);
     g_launches++;
 }
 
