@@ -58,6 +58,105 @@ __device__ __forceinline__ long long warp_p(long long base, int it) {
     return base + (long long)(threadIdx.x >> 5) * kSub + it * 32 + (threadIdx.x & 31);
 }
 
+// The list/count kernels: one block of kLT threads per chunk; thread t owns
+// particles [base + kPer t, base + kPer (t+1)) of its chunk (thread order =
+// index order) and reads their class bytes with kPer/16 16-byte loads.  Many
+// small blocks per SM keep enough chunks in flight (the work is latency-bound).
+static constexpr int kLT = 256;
+static constexpr int kPer = kChunk / kLT;  // 64 particles per thread
+static_assert(kPer == 64, "four uint4 of class bytes per thread");
+
+// class bytes of [p0, p0 + kPer) as 16 packed words (zero past n)
+__device__ __forceinline__ void load_cls(const unsigned char* __restrict__ cls, long long n, long long p0,
+                                         unsigned w[kPer / 4]) {
+    if (p0 + kPer <= n) {
+#pragma unroll
+        for (int u = 0; u < kPer / 16; u++) {
+            const uint4 v = *reinterpret_cast<const uint4*>(cls + p0 + 16 * u);
+            w[4 * u] = v.x; w[4 * u + 1] = v.y; w[4 * u + 2] = v.z; w[4 * u + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < kPer / 4; i++) {
+            unsigned x = 0;
+            for (int b = 0; b < 4; b++) {
+                const long long p = p0 + 4 * i + b;
+                if (p < n) x |= (unsigned)cls[p] << (8 * b);
+            }
+            w[i] = x;
+        }
+    }
+}
+
+// per-byte flag words (0xff / 0x00) -> one bit per byte
+__device__ __forceinline__ unsigned long long flags_to_bits(unsigned f, int i) {
+    const unsigned b = ((f >> 7) & 1u) | ((f >> 14) & 2u) | ((f >> 21) & 4u) | ((f >> 28) & 8u);
+    return (unsigned long long)b << (4 * i);
+}
+// bits of the class bytes equal to v (KIND 0), nonzero (KIND 1), zero (KIND 2)
+template <int KIND>
+__device__ __forceinline__ unsigned long long cls_bits(const unsigned w[kPer / 4], unsigned v = 0) {
+    unsigned long long m = 0;
+#pragma unroll
+    for (int i = 0; i < kPer / 4; i++) {
+        const unsigned f = KIND == 0 ? __vcmpeq4(w[i], v * 0x01010101u)
+                         : KIND == 1 ? __vcmpne4(w[i], 0u)
+                                     : __vcmpeq4(w[i], 0u);
+        m |= flags_to_bits(f, i);
+    }
+    return m;
+}
+// bits q with lo <= p0 + q < hi
+__device__ __forceinline__ unsigned long long range_bits(long long p0, long long lo, long long hi) {
+    const long long a = min(max(lo - p0, 0LL), (long long)kPer), b = min(max(hi - p0, 0LL), (long long)kPer);
+    if (b <= a) return 0ull;
+    const unsigned long long top = b == 64 ? ~0ull : ((1ull << b) - 1ull);
+    const unsigned long long bot = a == 64 ? ~0ull : ((1ull << a) - 1ull);
+    return top & ~bot;
+}
+
+// exclusive scan of one value per thread over the block (index order) and the
+// block total; all threads call it
+__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* sw, unsigned* total) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    unsigned x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sw[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        const unsigned t = lane < nw ? sw[lane] : 0u;
+        unsigned y = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned u = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += u;
+        }
+        if (lane < nw) sw[lane] = y - t;
+        if (lane == 31) sw[32] = y;
+    }
+    __syncthreads();
+    const unsigned off = sw[w] + x - v;
+    *total = sw[32];
+    __syncthreads();
+    return off;
+}
+
+// write p0 + (bit positions of m) to out[off..]
+__device__ __forceinline__ void emit_bits(unsigned long long m, long long p0, unsigned* __restrict__ out,
+                                          unsigned off) {
+    while (m) {
+        const int q = __ffsll((long long)m) - 1;
+        out[off++] = (unsigned)(p0 + q);
+        m &= m - 1;
+    }
+}
+
+
+
 // H-2: radial domain of a gyrocentre radius r = sqrt(2 psi) (IEEE sqrt and
 // exact comparisons against the ring radii of the window boundaries)
 __device__ __forceinline__ int radial_domain(const Geo& g, double psi) {
@@ -115,27 +214,24 @@ __global__ void __launch_bounds__(kShiftBlock) k_shift_classify(Geo g, const dou
 }
 
 // holes: movers at p < n_keep; fillers: keepers at p >= n_keep (per chunk)
-__global__ void __launch_bounds__(kShiftBlock) k_shift_count_holes(const unsigned char* __restrict__ cls, long long n,
+__global__ void __launch_bounds__(kLT) k_shift_count_holes(const unsigned char* __restrict__ cls, long long n,
                                                                    const long long* __restrict__ nkeep_p,
                                                                    unsigned* __restrict__ cntH,
                                                                    unsigned* __restrict__ cntF) {
     __shared__ unsigned sw[33];
     const long long nkeep = *nkeep_p;
-    const long long base = (long long)blockIdx.x * kChunk;
-    unsigned a = 0, b = 0;
-#pragma unroll
-    for (int it = 0; it < kIt; it++) {
-        long long p = warp_p(base, it);
-        unsigned char c = (p < n) ? cls[p] : 0;
-        a += __popc(__ballot_sync(0xffffffffu, (p < n) && (p < nkeep) && c != 0));
-        b += __popc(__ballot_sync(0xffffffffu, (p < n) && (p >= nkeep) && c == 0));
-    }
-    unsigned ta, tb;
-    warp_offsets(a, sw, &ta);
-    warp_offsets(b, sw, &tb);
+    const long long ch = blockIdx.x;
+    const long long p0 = ch * kChunk + (long long)threadIdx.x * kPer;
+    unsigned w[kPer / 4];
+    load_cls(cls, n, p0, w);
+    const unsigned h = __popcll(cls_bits<1>(w) & range_bits(p0, 0, min(n, nkeep)));
+    const unsigned f = __popcll(cls_bits<2>(w) & range_bits(p0, nkeep, n));
+    unsigned th, tf;
+    block_excl_scan(h, sw, &th);
+    block_excl_scan(f, sw, &tf);
     if (threadIdx.x == 0) {
-        cntH[blockIdx.x] = ta;
-        cntF[blockIdx.x] = tb;
+        cntH[ch] = th;
+        cntF[ch] = tf;
     }
 }
 
@@ -148,37 +244,23 @@ struct ShiftAttrs {
 // movers -> index lists (left list, right list), in index order
 // (deterministic); the attribute copies run in k_shift_copy with one thread
 // per (particle, attribute) so the sparse reads are all in flight at once.
-__global__ void __launch_bounds__(kShiftBlock) k_shift_pack(const unsigned char* __restrict__ cls, long long n,
+__global__ void __launch_bounds__(kLT) k_shift_pack(const unsigned char* __restrict__ cls, long long n,
                                                             const unsigned* __restrict__ offL,
                                                             const unsigned* __restrict__ offR,
                                                             unsigned* __restrict__ idxL, unsigned* __restrict__ idxR) {
     __shared__ unsigned sw[33];
-    const long long base = (long long)blockIdx.x * kChunk;
-    const int lane = threadIdx.x & 31;
-    unsigned mL[kIt], mR[kIt];
-    unsigned a = 0, b = 0;
-#pragma unroll
-    for (int it = 0; it < kIt; it++) {
-        long long p = warp_p(base, it);
-        unsigned char c = (p < n) ? cls[p] : 0;
-        mL[it] = __ballot_sync(0xffffffffu, c == 1);
-        mR[it] = __ballot_sync(0xffffffffu, c == 2);
-        a += __popc(mL[it]);
-        b += __popc(mR[it]);
-    }
+    const long long ch = blockIdx.x;
+    const long long p0 = ch * kChunk + (long long)threadIdx.x * kPer;
+    unsigned w[kPer / 4];
+    load_cls(cls, n, p0, w);
+    const unsigned long long in = range_bits(p0, 0, n);
+    const unsigned long long mL = cls_bits<0>(w, 1u) & in;
+    const unsigned long long mR = cls_bits<0>(w, 2u) & in;
     unsigned t;
-    unsigned ol = offL[blockIdx.x] + warp_offsets(a, sw, &t);
-    unsigned orr = offR[blockIdx.x] + warp_offsets(b, sw, &t);
-    if (a + b == 0) return;
-    const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int it = 0; it < kIt; it++) {
-        const unsigned p = (unsigned)warp_p(base, it);
-        if ((mL[it] >> lane) & 1) idxL[ol + __popc(mL[it] & lt)] = p;
-        if ((mR[it] >> lane) & 1) idxR[orr + __popc(mR[it] & lt)] = p;
-        ol += __popc(mL[it]);
-        orr += __popc(mR[it]);
-    }
+    const unsigned ol = offL[ch] + block_excl_scan(__popcll(mL), sw, &t);
+    const unsigned orr = offR[ch] + block_excl_scan(__popcll(mR), sw, &t);
+    emit_bits(mL, p0, idxL, ol);
+    emit_bits(mR, p0, idxR, orr);
 }
 
 // dst.a[d][q] = src.a[d][idx[q]] (gather; dst contiguous) or, with scatter,
@@ -206,62 +288,40 @@ __global__ void k_shift_copy(ShiftAttrs src, ShiftAttrs dst, const unsigned* __r
 }
 
 // list hole positions in index order
-__global__ void __launch_bounds__(kShiftBlock) k_shift_list_holes(const unsigned char* __restrict__ cls, long long n,
+__global__ void __launch_bounds__(kLT) k_shift_list_holes(const unsigned char* __restrict__ cls, long long n,
                                                                   const long long* __restrict__ nkeep_p,
                                                                   const unsigned* __restrict__ offH,
                                                                   unsigned* __restrict__ holes) {
     __shared__ unsigned sw[33];
     const long long nkeep = *nkeep_p;
-    const long long base = (long long)blockIdx.x * kChunk;
-    if (base >= nkeep) return;  // no holes in this chunk (uniform per block)
-    const int lane = threadIdx.x & 31;
-    unsigned m[kIt];
-    unsigned a = 0;
-#pragma unroll
-    for (int it = 0; it < kIt; it++) {
-        long long p = warp_p(base, it);
-        bool hole = (p < n) && (p < nkeep) && cls[p] != 0;
-        m[it] = __ballot_sync(0xffffffffu, hole);
-        a += __popc(m[it]);
-    }
+    const long long ch = blockIdx.x;
+    if (ch * kChunk >= nkeep) return;  // holes lie below n_keep (uniform per block)
+    const long long p0 = ch * kChunk + (long long)threadIdx.x * kPer;
+    unsigned w[kPer / 4];
+    load_cls(cls, n, p0, w);
+    const unsigned long long m = cls_bits<1>(w) & range_bits(p0, 0, min(n, nkeep));
     unsigned t;
-    unsigned oh = offH[blockIdx.x] + warp_offsets(a, sw, &t);
-    if (a == 0) return;
-#pragma unroll
-    for (int it = 0; it < kIt; it++) {
-        if ((m[it] >> lane) & 1) holes[oh + __popc(m[it] & ((1u << lane) - 1u))] = (unsigned)warp_p(base, it);
-        oh += __popc(m[it]);
-    }
+    const unsigned o = offH[ch] + block_excl_scan(__popcll(m), sw, &t);
+    emit_bits(m, p0, holes, o);
 }
 
 // list tail-keeper (filler) positions in index order; the k-th filler moves
 // into the k-th hole (k_shift_copy with scatter)
-__global__ void __launch_bounds__(kShiftBlock) k_shift_list_fill(const unsigned char* __restrict__ cls, long long n,
+__global__ void __launch_bounds__(kLT) k_shift_list_fill(const unsigned char* __restrict__ cls, long long n,
                                                                  const long long* __restrict__ nkeep_p,
                                                                  const unsigned* __restrict__ offF,
                                                                  unsigned* __restrict__ fills) {
     __shared__ unsigned sw[33];
     const long long nkeep = *nkeep_p;
-    const long long base = (long long)blockIdx.x * kChunk;
-    if (base + kChunk <= nkeep) return;  // no fillers in this chunk (uniform per block)
-    const int lane = threadIdx.x & 31;
-    unsigned m[kIt];
-    unsigned a = 0;
-#pragma unroll
-    for (int it = 0; it < kIt; it++) {
-        long long p = warp_p(base, it);
-        bool fill = (p < n) && (p >= nkeep) && cls[p] == 0;
-        m[it] = __ballot_sync(0xffffffffu, fill);
-        a += __popc(m[it]);
-    }
+    const long long ch = blockIdx.x;
+    if ((ch + 1) * kChunk <= nkeep) return;  // fillers lie at or above n_keep (uniform per block)
+    const long long p0 = ch * kChunk + (long long)threadIdx.x * kPer;
+    unsigned w[kPer / 4];
+    load_cls(cls, n, p0, w);
+    const unsigned long long m = cls_bits<2>(w) & range_bits(p0, nkeep, n);
     unsigned t;
-    unsigned of = offF[blockIdx.x] + warp_offsets(a, sw, &t);
-    if (a == 0) return;
-#pragma unroll
-    for (int it = 0; it < kIt; it++) {
-        if ((m[it] >> lane) & 1) fills[of + __popc(m[it] & ((1u << lane) - 1u))] = (unsigned)warp_p(base, it);
-        of += __popc(m[it]);
-    }
+    const unsigned o = offF[ch] + block_excl_scan(__popcll(m), sw, &t);
+    emit_bits(m, p0, fills, o);
 }
 
 // n_keep = n - (total left + total right), written on the device
@@ -292,8 +352,7 @@ void launch_shift_nkeep(long long n, const unsigned* totL, const unsigned* totR,
 
 void launch_shift_count_holes(const unsigned char* cls, long long n, const long long* nkeep, unsigned* cntH,
                               unsigned* cntF, cudaStream_t st) {
-    int nb = shift_chunks(n);
-    k_shift_count_holes<<<nb, kShiftBlock, 0, st>>>(cls, n, nkeep, cntH, cntF);
+    k_shift_count_holes<<<shift_chunks(n), kLT, 0, st>>>(cls, n, nkeep, cntH, cntF);
     g_launches++;
 }
 
@@ -309,10 +368,9 @@ void launch_shift_pack(double* const* attrs, int nattr, unsigned long long* id, 
                        const unsigned* offL, const unsigned* offR, double* const* sendL, double* const* sendR,
                        unsigned long long* idL, unsigned long long* idR, unsigned* idx, long long nL, long long nR,
                        cudaStream_t st) {
-    int nb = shift_chunks(n);
     unsigned* idxL = idx;
     unsigned* idxR = idx + nL;
-    k_shift_pack<<<nb, kShiftBlock, 0, st>>>(cls, n, offL, offR, idxL, idxR);
+    k_shift_pack<<<shift_chunks(n), kLT, 0, st>>>(cls, n, offL, offR, idxL, idxR);
     g_launches++;
     ShiftAttrs A = mk(attrs, nattr, id);
     for (int side = 0; side < 2; side++) {
@@ -333,10 +391,10 @@ void launch_shift_pack(double* const* attrs, int nattr, unsigned long long* id, 
 void launch_shift_backfill(double* const* attrs, int nattr, unsigned long long* id, const unsigned char* cls,
                            long long n, const long long* nkeep, const unsigned* offH, const unsigned* offF,
                            unsigned* holes, unsigned* fills, long long nholes, cudaStream_t st) {
-    int nb = shift_chunks(n);
-    const unsigned* nholes_dev = offH + nb;  // scan total = number of holes
-    k_shift_list_holes<<<nb, kShiftBlock, 0, st>>>(cls, n, nkeep, offH, holes);
-    k_shift_list_fill<<<nb, kShiftBlock, 0, st>>>(cls, n, nkeep, offF, fills);
+    const int nchunk = shift_chunks(n);
+    const unsigned* nholes_dev = offH + nchunk;  // scan total = number of holes
+    k_shift_list_holes<<<nchunk, kLT, 0, st>>>(cls, n, nkeep, offH, holes);
+    k_shift_list_fill<<<nchunk, kLT, 0, st>>>(cls, n, nkeep, offF, fills);
     g_launches += 2;
     if (nholes > 0) {
         ShiftAttrs A = mk(attrs, nattr, id);
