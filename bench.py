@@ -241,6 +241,17 @@ def run_gpu(args):
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
         traffic = tr.get(size, {}).get(dom)
+        # the deposit's own roof: shared-memory atomic wavefronts (one per clock
+        # per SM; ncu count per launch at this configuration) over its live time
+        wf = tr.get(size, {}).get("charge_deposit", {}).get("smem_atomic_wavefronts_per_launch")
+        if wf and "charge_deposit" in roof:
+            props = torch.cuda.get_device_properties(local)
+            clk_hz = (clk.summary() or {}).get("sm_mhz") or 1965.0
+            peak_wf = props.multi_processor_count * clk_hz * 1e6
+            ach = wf / (roof["charge_deposit"]["avg_ms"] * 1e-3)
+            roof["charge_deposit"]["smem_atomic"] = {
+                "achieved_wavefronts_per_s": ach, "peak_wavefronts_per_s": peak_wf, "frac": ach / peak_wf,
+                "wavefronts_per_launch": wf, "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom"}
     except Exception:
         pass
     # end to end through the C ABI with HOST buffers (pinned): H2D state, step, D2H state
