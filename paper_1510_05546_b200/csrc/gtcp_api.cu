@@ -472,25 +472,6 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     }
     gtcp::launch_tile_spans(c->geo, c->dep_cap_nodes, c->tile_span, c->st);
     c->launches0 = gtcp::g_launches;
-    // optional: L2 persisting window on the gather field (measured: push 7% slower
-    // than plain evict-first particle streams, so off by default)
-    if (c->st && getenv("GTCP_L2PERSIST")) {  // measured slower on B200 (opt-in only)
-        int max_persist = 0, max_window = 0;
-        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device);
-        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
-        size_t want = (size_t)P * mg * 6 * sizeof(double);
-        if (max_persist > 0 && max_window > 0) {
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(want, (size_t)max_persist));
-            cudaStreamAttrValue v = {};
-            v.accessPolicyWindow.base_ptr = c->gfield;
-            v.accessPolicyWindow.num_bytes = std::min<size_t>(want, (size_t)max_window);
-            v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)max_persist / (float)std::max<size_t>(want, 1));
-            v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-            v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-            cudaStreamSetAttribute(c->st, cudaStreamAttributeAccessPolicyWindow, &v);
-        }
-        cudaGetLastError();  // best effort
-    }
     // NCCL communicators
     if (nranks > 1) {
         ncclUniqueId uid;
@@ -799,35 +780,15 @@ extern "C" gtcp_status gtcp_field(gtcp_ctx c) {
 // push over [0, n): the binned part tile by tile (field windows staged in
 // shared memory), the tail (shift arrivals beyond the last bin) plainly
 static void push_range(gtcp_ctx c, double* const* src, double* const* base, double* const* out, double h) {
-    // the tile-staged push (field windows in shared memory) measured 2x slower
-    // than the plain fused push on B200: opt-in only
-    static const bool tiled = [] {
-        const char* e = getenv("GTCP_PUSH_TILED");
-        return e && e[0] == '1';
-    }();
-    long long tiled_end = 0;
-    if (tiled && !c->geo.prec32 && c->charge_mode == 0 && c->n_binned > 0) {
-        tiled_end = std::min(c->n, c->n_binned);
-        launch_push_tiled(c->geo, src, base, out, c->mu, tiled_end, h, c->gfield, c->tiles, c->dc, c->st);
-    }
-    // fused toroidal classification for the shift that follows (plain kernel only)
-    const bool fuse = c->prm.ntoroidal > 1 && tiled_end == 0 && c->cls != nullptr;
+    // fused toroidal classification for the shift that follows
+    const bool fuse = c->prm.ntoroidal > 1 && c->cls != nullptr;
     unsigned* cntL = c->bcount;
     unsigned* cntR = cntL + (c->shift_blocks + 1);
     if (fuse) CU_VOID(cudaMemsetAsync(cntL, 0, 2 * (c->shift_blocks + 1) * sizeof(unsigned), c->st));
     c->cls_ready = fuse;
-    if (c->n > tiled_end) {
-        const double* s2[5];
-        const double* b2[5];
-        double* o2[5];
-        for (int d = 0; d < 5; d++) {
-            s2[d] = pofs(src[d], tiled_end);
-            b2[d] = pofs(base[d], tiled_end);
-            o2[d] = pofs(out[d], tiled_end);
-        }
-        launch_push3(c->geo, s2, b2, o2, pofs(c->mu, tiled_end), c->n - tiled_end, h, c->gfield, c->dc, c->st,
-                     fuse ? c->cls : nullptr, fuse ? cntL : nullptr, fuse ? cntR : nullptr);
-    }
+    if (c->n > 0)
+        launch_push3(c->geo, src, base, out, c->mu, c->n, h, c->gfield, c->dc, c->st, fuse ? c->cls : nullptr,
+                     fuse ? cntL : nullptr, fuse ? cntR : nullptr);
 }
 
 extern "C" gtcp_status gtcp_push(gtcp_ctx c, int stage) {

@@ -99,9 +99,6 @@ void launch_fx_to_real(const Geo& g, const long long* fx, double* rho, const Dev
 void launch_push3(const Geo& g, const double* const src[5], const double* const base[5], double* const out[5],
                   const double* mu, long long n, double h, const double* gfield, DevCounters* dc, cudaStream_t st,
                   unsigned char* cls = nullptr, unsigned* cntL = nullptr, unsigned* cntR = nullptr);
-void launch_push_tiled(const Geo& g, const double* const src[5], const double* const base[5], double* const out[5],
-                       const double* mu, long long n, double h, const double* gfield, const Tile* tiles,
-                       DevCounters* dc, cudaStream_t st);
 void launch_wmax(const double* w, long long n, DevCounters* dc, cudaStream_t st);
 void launch_bin_keys(const Geo& g, const PSet& s, long long n, unsigned* key, unsigned* rank, unsigned* count,
                      cudaStream_t st);

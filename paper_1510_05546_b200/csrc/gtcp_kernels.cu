@@ -737,21 +737,11 @@ __device__ __forceinline__ double warp_max(double v) {
 // One RK2 stage of one particle (U-1..U-8): returns the new state X[5] from
 // the source state (psi, theta, zeta, rho_par, w), mu and the base state.
 // Counts reflections / plane clamps into the caller's registers.
-// default gather source: the interval-interleaved field in global memory
-struct GlobalFetch {
-    const double* gf;
-    long long mgrid;
-    __device__ __forceinline__ const double* operator()(int k, int m, int j, int mt, int node) const {
-        (void)m; (void)j; (void)mt;
-        return gf + ((long long)k * mgrid + node) * 6;
-    }
-};
-
-template <int GU = 8, class Fetch = GlobalFetch>
+template <int GU = 8>
 __device__ __forceinline__ void push_one(const Geo& g, const RingTab* __restrict__ rt, double psi, double theta,
                                          double zeta, double rho_par, double w, double mu, const double* base,
                                          double h, const double* __restrict__ gf, double* X, long long& refl,
-                                         long long& clamps, const Fetch* fetch = nullptr) {
+                                         long long& clamps) {
     // U-1
     double st, ct;
     sincos_theta(theta, &st, &ct);
@@ -769,7 +759,7 @@ __device__ __forceinline__ void push_one(const Geo& g, const RingTab* __restrict
     if (k < 0 || k > g.P - 1) { clamps++; k = min(max(k, 0), g.P - 1); }
     const double wz0 = 1.0 - wz1;
     // phase 1: the 8 (gyro-point, ring) stencil records (ring tables in smem)
-    int node[8], mrec[8], jrec[8], mtrec[8];
+    int node[8];
     double wa[8], wb[8];
     {
         const double rho_r = rho * inv_r;
@@ -794,9 +784,6 @@ __device__ __forceinline__ void push_one(const Geo& g, const RingTab* __restrict
                 const double wt1 = s - (double)j;
                 const double wp = mm ? wp1 : 1.0 - wp1;
                 node[2 * l + mm] = t.igrid + j;
-                mrec[2 * l + mm] = i + mm;
-                jrec[2 * l + mm] = j;
-                mtrec[2 * l + mm] = t.mtheta;
                 wa[2 * l + mm] = wp * (1.0 - wt1);
                 wb[2 * l + mm] = wp * wt1;
             }
@@ -808,8 +795,7 @@ __device__ __forceinline__ void push_one(const Geo& g, const RingTab* __restrict
     const double* gk = gf + (long long)k * g.mgrid * 6;
 #pragma unroll GU
     for (int q = 0; q < 8; q++) {
-        const double2* qq = reinterpret_cast<const double2*>(
-            fetch ? (*fetch)(k, mrec[q], jrec[q], mtrec[q], node[q]) : gk + (long long)node[q] * 6);
+        const double2* qq = reinterpret_cast<const double2*>(gk + (long long)node[q] * 6);
         const double2 v0 = qq[0], v1 = qq[1], v2 = qq[2];
         const double2 v3 = qq[3], v4 = qq[4], v5 = qq[5];
         const double a0 = wa[q], a1 = wb[q];
@@ -934,293 +920,6 @@ __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long lon
     push_epilogue(dc, wmax, refl, clamps, nonfinite);
 }
 
-// ---------------------------------------------------------------------------
-// TMA-staged push: persistent CTAs stream chunks of kPC particles; one thread
-// issues cp.async.bulk copies of the chunk's SoA segments (6 arrays for stage
-// 1, 11 for stage 2) into a kNB-deep ring of shared-memory stage buffers with
-// mbarrier completion, so the particle streams' HBM latency overlaps the
-// previous chunks' gather + RHS work.
-// ---------------------------------------------------------------------------
-static constexpr int kPC = 256;  // particles per chunk (= threads per CTA)
-static constexpr int kNB = 4;    // stage buffers
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-    unsigned ok = 0;
-    while (!ok) {
-        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                     : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-    }
-}
-
-template <int NARR>
-__global__ void __launch_bounds__(kPC, 2) k_push_tma(Geo g, PushPtrs pp, long long n, double h,
-                                                     const double* __restrict__ gf, DevCounters* dc) {
-    // NARR = 6: src 5 + mu (stage 1, base == src); NARR = 11: + base 5 (stage 2)
-    extern __shared__ __align__(128) double sbuf[];  // [kNB][NARR][kPC], then the ring table
-    __shared__ __align__(8) unsigned long long full[kNB];
-    RingTab* rt = reinterpret_cast<RingTab*>(sbuf + (size_t)kNB * NARR * kPC);
-    load_ring_tab(g, rt);
-    const long long nchunks = (n + kPC - 1) / kPC;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kNB; s++) mbar_init(&full[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    auto issue = [&](long long c, int s) {
-        const long long p0 = c * kPC;
-        const long long cnt = min((long long)kPC, n - p0);
-        const unsigned bytes = (unsigned)(((cnt * 8) + 15) & ~15LL);  // arrays are padded to 256 elements
-        mbar_expect_tx(&full[s], bytes * NARR);
-        double* dst = sbuf + (size_t)s * NARR * kPC;
-#pragma unroll
-        for (int a = 0; a < NARR; a++) {
-            const double* src = a < 5 ? pp.src[a] : (a == 5 ? pp.mu : pp.base[a - 6]);
-            bulk_g2s(dst + a * kPC, src + p0, bytes, &full[s]);
-        }
-    };
-    if (threadIdx.x == 0)
-        for (int s = 0; s < kNB; s++) {
-            long long c = blockIdx.x + (long long)s * gridDim.x;
-            if (c < nchunks) issue(c, s);
-        }
-    double wmax = 0.0;
-    long long refl = 0, clamps = 0;
-    int nonfinite = 0;
-    int it = 0;
-    for (long long c = blockIdx.x; c < nchunks; c += gridDim.x, it++) {
-        const int s = it % kNB;
-        mbar_wait(&full[s], (unsigned)((it / kNB) & 1));
-        const double* sb = sbuf + (size_t)s * NARR * kPC;
-        const long long p = c * kPC + threadIdx.x;
-        if (p < n) {
-            const int t = threadIdx.x;
-            double base[5], X[5];
-#pragma unroll
-            for (int d = 0; d < 5; d++) base[d] = (NARR == 11) ? sb[(6 + d) * kPC + t] : sb[d * kPC + t];
-            push_one(g, rt, sb[0 * kPC + t], sb[1 * kPC + t], sb[2 * kPC + t], sb[3 * kPC + t], sb[4 * kPC + t],
-                     sb[5 * kPC + t], base, h, gf, X, refl, clamps);
-            if (!(isfinite(X[0]) && isfinite(X[1]) && isfinite(X[2]) && isfinite(X[3]) && isfinite(X[4])))
-                nonfinite = 1;
-#pragma unroll
-            for (int d = 0; d < 5; d++) pp.out[d][p] = X[d];
-            wmax = fmax(wmax, fabs(X[4]));
-        }
-        __syncthreads();  // everyone is done with buffer s: refill it
-        if (threadIdx.x == 0) {
-            long long cn = c + (long long)kNB * gridDim.x;
-            if (cn < nchunks) issue(cn, s);
-        }
-    }
-    push_epilogue(dc, wmax, refl, clamps, nonfinite);
-}
-
-// ---------------------------------------------------------------------------
-// Tile-based push: persistent CTAs take the cell-sorted tiles of the charge;
-// for each chunk of 256 markers the CTA stages the field windows (intervals
-// present in the chunk x ring band x label window, 48 B per node: both
-// bounding planes x 3 components) into shared memory with coalesced 16-byte
-// loads, then every gather reads there (global fallback outside the window).
-// ---------------------------------------------------------------------------
-struct WindowFetch {
-    const double* win;   // smem: [slot][column][6]
-    const int* js;       // smem: [interval][kMaxRings]
-    const int* slot_of;  // smem: [interval] -> staged slot or -1
-    const int2* WO;      // smem: [ring of band] (width, column offset)
-    int m_lo, nr, S;
-    const double* gf;
-    long long mgrid;
-    __device__ __forceinline__ const double* operator()(int k, int m, int j, int mt, int node) const {
-        const int s = slot_of[k];
-        const int q = m - m_lo;
-        if (s >= 0 && (unsigned)q < (unsigned)nr) {
-            int d = j - js[k * kMaxRings + q];
-            d += (d < 0) ? mt : 0;
-            const int2 wo = WO[q];
-            // nodes j and j+1 must both be in the window and adjacent in smem
-            if ((unsigned)d + 1u < (unsigned)wo.x) return win + ((long long)s * S + wo.y + d) * 6;
-        }
-        return gf + ((long long)k * mgrid + node) * 6;
-    }
-};
-
-template <bool CS>
-__global__ void __launch_bounds__(256, 2) k_push_tiled(Geo g, PushPtrs pp, long long n, double h,
-                                                       const double* __restrict__ gf, const Tile* __restrict__ tiles,
-                                                       const int* ntiles_p, int* tile_next, DevCounters* dc,
-                                                       double rho_cut, int win_nodes_cap) {
-    extern __shared__ __align__(16) double smem_push[];
-    double* win = smem_push;                                                   // [win_nodes_cap][6]
-    RingTab* rt = reinterpret_cast<RingTab*>(win + (size_t)win_nodes_cap * 6);
-    int* js = reinterpret_cast<int*>(rt + (g.mpsi + 1));                         // [P][kMaxRings]
-    int* slot_of = js + g.P * kMaxRings;                                        // [P]
-    unsigned char* colq = reinterpret_cast<unsigned char*>(slot_of + g.P);      // [S]
-    __shared__ int2 WO[kMaxRings];
-    __shared__ int s_mt[kMaxRings];
-    __shared__ int s_m_lo, s_nr, s_S, s_ni, s_tile, s_nslot;
-    __shared__ unsigned s_mask[2];
-    __shared__ int s_slot_k[64];
-    load_ring_tab(g, rt);
-    const int ntiles = *ntiles_p;
-    double wmax = 0.0;
-    long long refl = 0, clamps = 0;
-    int nonfinite = 0;
-    auto ld = [&](const double* a, long long p) { return CS ? __ldcs(a + p) : a[p]; };
-    for (;;) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(tile_next, 1);
-        __syncthreads();
-        const int t = s_tile;
-        if (t >= ntiles) break;
-        const Tile tl = tiles[t];
-        if (threadIdx.x == 0) {
-            const int i = tl.ring;
-            const int hh = win_halo(g, rho_cut);
-            const int m_lo = max(0, i - hh), m_hi = min(g.mpsi, i + 1 + hh);
-            int S = 0;
-            for (int q = 0; q < m_hi - m_lo + 1; q++) {
-                int W = win_width(g, i, tl.c0, tl.c1, m_lo + q, rho_cut);
-                WO[q] = make_int2(W, S);
-                s_mt[q] = rt[m_lo + q].mtheta;
-                S += W;
-            }
-            s_m_lo = m_lo;
-            s_nr = m_hi - m_lo + 1;
-            s_S = S;
-            s_ni = (S > 0) ? min(g.P, min(64, win_nodes_cap / S)) : 0;
-        }
-        __syncthreads();
-        const int m_lo = s_m_lo, nr = s_nr, S = s_S, ni = s_ni;
-        {
-            const int i = tl.ring;
-            const int mti = rt[i].mtheta;
-            const double fc = 0.5 * (double)(tl.c0 + tl.c1 + 1) / mti;
-            for (int e = threadIdx.x; e < g.P * nr; e += blockDim.x) {
-                int kk = e / nr, q = e - kk * nr;
-                int m = m_lo + q;
-                int mt = s_mt[q];
-                double dq;
-                double hw = win_halfwidth(g, i, tl.c0, tl.c1, m, rho_cut, &dq);
-                double zk = (double)(g.k0 + kk) * g.dzeta;
-                double f = fc + zk * dq - hw;
-                f = f - floor(f);
-                js[kk * kMaxRings + q] = min(max((int)floor(f * mt), 0), mt - 1);
-            }
-            for (int q = 0; q < nr; q++)
-                for (int x = threadIdx.x; x < WO[q].x; x += blockDim.x) colq[WO[q].y + x] = (unsigned char)q;
-        }
-        const long long tend = min(tl.end, n);
-        for (long long c0 = tl.start; c0 < tend; c0 += blockDim.x) {
-            const long long p = c0 + threadIdx.x;
-            const bool act = p < tend;
-            double src[6], base[5];
-            int k = 0;
-            if (act) {
-#pragma unroll
-                for (int d = 0; d < 5; d++) src[d] = ld(pp.src[d], p);
-                src[5] = ld(pp.mu, p);
-#pragma unroll
-                for (int d = 0; d < 5; d++) base[d] = (pp.base[d] == pp.src[d]) ? src[d] : ld(pp.base[d], p);
-                double wz1;
-                k = min(max(plane_of(g, src[2], &wz1) - g.k0, 0), g.P - 1);
-            }
-            if (threadIdx.x < 2) s_mask[threadIdx.x] = 0u;
-            __syncthreads();  // also: previous chunk done with the window buffer
-            if (act) atomicOr(&s_mask[k >> 5], 1u << (k & 31));
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                int ns = 0;
-                for (int kk = 0; kk < g.P; kk++) slot_of[kk] = -1;
-                for (int w = 0; w < 2; w++) {
-                    unsigned mk = s_mask[w];
-                    while (mk && ns < ni) {
-                        int b = __ffs(mk) - 1;
-                        mk &= mk - 1;
-                        slot_of[w * 32 + b] = ns;
-                        s_slot_k[ns] = w * 32 + b;
-                        ns++;
-                    }
-                }
-                s_nslot = ns;
-            }
-            __syncthreads();
-            // stage the windows: (slot, column, 16-byte part) -> coalesced 16-byte copies
-            const int ns = s_nslot;
-            const int total = ns * S * 3;
-            for (int e = threadIdx.x; e < total; e += blockDim.x) {
-                const int part = e % 3;
-                const int col = (e / 3) % S;
-                const int s = e / (3 * S);
-                const int q = colq[col];
-                const int kk = s_slot_k[s];
-                const int mt = s_mt[q];
-                int jn = js[kk * kMaxRings + q] + (col - WO[q].y);
-                if (jn >= mt) jn -= mt;
-                const double2* srcp = reinterpret_cast<const double2*>(
-                    gf + ((long long)kk * g.mgrid + rt[m_lo + q].igrid + jn) * 6) + part;
-                reinterpret_cast<double2*>(win + ((long long)s * S + col) * 6)[part] = __ldg(srcp);
-            }
-            __syncthreads();
-            if (act) {
-                WindowFetch F{win, js, slot_of, WO, m_lo, nr, S, gf, g.mgrid};
-                double X[5];
-                push_one<8, WindowFetch>(g, rt, src[0], src[1], src[2], src[3], src[4], src[5], base, h, gf, X,
-                                         refl, clamps, &F);
-                if (!(isfinite(X[0]) && isfinite(X[1]) && isfinite(X[2]) && isfinite(X[3]) && isfinite(X[4])))
-                    nonfinite = 1;
-#pragma unroll
-                for (int d = 0; d < 5; d++) {
-                    if (CS) __stcs(pp.out[d] + p, X[d]);
-                    else pp.out[d][p] = X[d];
-                }
-                wmax = fmax(wmax, fabs(X[4]));
-            }
-        }
-        __syncthreads();
-    }
-    push_epilogue(dc, wmax, refl, clamps, nonfinite);
-}
-
-static int g_push_win_cap = 0;
-size_t push_tiled_smem(const Geo& g, int win_cap) {
-    return (size_t)win_cap * 48 + (g.mpsi + 1) * sizeof(RingTab) + (size_t)g.P * kMaxRings * 4 + g.P * 4 + 4096 + 64;
-}
-
-void launch_push_tiled(const Geo& g, const double* const src[5], const double* const base[5], double* const out[5],
-                       const double* mu, long long n, double h, const double* gfield, const Tile* tiles,
-                       DevCounters* dc, cudaStream_t st) {
-    PushPtrs pp;
-    for (int d = 0; d < 5; d++) {
-        pp.src[d] = src[d];
-        pp.base[d] = base[d];
-        pp.out[d] = out[d];
-    }
-    pp.mu = mu;
-    pp.cls = nullptr;
-    pp.cntL = pp.cntR = nullptr;
-    const int win_cap = 1024;  // nodes of 48 B: 48 KB of windows per CTA
-    size_t sm = push_tiled_smem(g, win_cap);
-    static bool cfg = (cudaFuncSetAttribute(k_push_tiled<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)std::max<size_t>(sm, 96 * 1024)) == cudaSuccess);
-    (void)cfg;
-    (void)g_push_win_cap;
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    cudaMemsetAsync(&dc->tile_next, 0, sizeof(int), st);
-    k_push_tiled<true><<<2 * nsm, 256, sm, st>>>(g, pp, n, h, gfield, tiles, &dc->ntiles, &dc->tile_next, dc,
-                                                 deposit_rho_cut(g), win_cap);
-    g_launches++;
-}
-
 void launch_push3(const Geo& g, const double* const src[5], const double* const base[5], double* const out[5],
                   const double* mu, long long n, double h, const double* gfield, DevCounters* dc,
                   cudaStream_t st, unsigned char* cls, unsigned* cntL, unsigned* cntR) {
@@ -1235,46 +934,13 @@ void launch_push3(const Geo& g, const double* const src[5], const double* const 
     pp.cls = cls;
     pp.cntL = cntL;
     pp.cntR = cntR;
-    static const int variant0 = [] {
-        const char* e = getenv("GTCP_PUSH_VARIANT");
-        return e ? atoi(e) : 4;
-    }();
-    int variant = variant0;
-    const bool stage2 = (base[0] != src[0]);
-    if (cls) variant = 4;  // fused classification lives in the plain kernel
-    if (g.prec32) {  // fp32 state: the plain fused kernel
-        int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
-        size_t smr = (g.mpsi + 1) * sizeof(RingTab);
-        k_push<2, true, 8, float><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
-    } else if (variant == 0) {
-        // TMA-staged persistent kernel, 2 CTAs per SM
-        int nsm = 148;
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-        long long nch = (n + kPC - 1) / kPC;
-        int blocks = (int)std::min<long long>(nch, 2LL * nsm);
-        if (stage2) {
-            size_t sm = (size_t)kNB * 11 * kPC * sizeof(double) + (g.mpsi + 1) * sizeof(RingTab);
-            static bool cfg = (cudaFuncSetAttribute(k_push_tma<11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    (int)sm) == cudaSuccess);
-            (void)cfg;
-            k_push_tma<11><<<blocks, kPC, sm, st>>>(g, pp, n, h, gfield, dc);
-        } else {
-            size_t sm = (size_t)kNB * 6 * kPC * sizeof(double) + (g.mpsi + 1) * sizeof(RingTab);
-            static bool cfg = (cudaFuncSetAttribute(k_push_tma<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    (int)sm) == cudaSuccess);
-            (void)cfg;
-            k_push_tma<6><<<blocks, kPC, sm, st>>>(g, pp, n, h, gfield, dc);
-        }
-    } else {
-        int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
-        size_t smr = (g.mpsi + 1) * sizeof(RingTab);
-        if (variant == 3) k_push<3, false><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
-        else if (variant == 4) k_push<2, true><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
-        else if (variant == 5) k_push<3, true, 2><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
-        else if (variant == 6) k_push<3, true, 4><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
-        else if (variant == 7) k_push<2, true, 4><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
-        else k_push<2, false><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
-    }
+    // one particle per thread, 2 CTAs of 256 per SM (128 registers); measured
+    // alternatives (3 CTAs, 96-register shapes, TMA- or smem-staged streams and
+    // field windows, a texture-path gather) were all slower
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
+    size_t smr = (g.mpsi + 1) * sizeof(RingTab);
+    if (g.prec32) k_push<2, true, 8, float><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
+    else k_push<2, true, 8, double><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
     g_launches++;
 }
 

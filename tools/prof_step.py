@@ -1,6 +1,6 @@
 """Short profiling / timing driver: load a class, run warm-up + timed steps,
 print per-phase CUDA-event times (ms per step).  Used for ncu captures and
-A/B experiments (env knobs: GTCP_PUSH_MINB)."""
+A/B experiments (env knobs: GTCP_DEPOSIT_CTAS, GTCP_PROFILE_BIN, GTCP_PROFILE_SHIFT)."""
 import argparse
 import json
 import os
