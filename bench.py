@@ -173,7 +173,11 @@ def run_gpu(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     size = args.size or ("A" if world == 1 else "B")
-    p = G.gtcp_default_params(size, ntoroidal=world, bin_every=args.bin_every)
+    over = {"micell": args.micell} if args.micell else {}
+    ntor = world // (args.nradial * args.npartdom)
+    assert ntor * args.nradial * args.npartdom == world, "GPUs must equal ntoroidal * nradial * npartdom"
+    p = G.gtcp_default_params(size, ntoroidal=ntor, nradial=args.nradial, npartdom=args.npartdom,
+                              bin_every=args.bin_every, precision=args.precision, **over)
     nccl_id = None
     if world > 1:
         obj = [G.gtcp_nccl_unique_id() if rank == 0 else None]
@@ -288,12 +292,15 @@ def run_gpu(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "state_storage": "f64" if args.precision == 64 else "f32 (arithmetic f64)",
             "data": "synthetic",
             "config": {"workload": f"GTC-P class {size}: mpsi={p.mpsi} mthetamax={p.mthetamax} "
                                    f"mzetamax={p.mzetamax} micell={p.micell}",
                        "particles": n_total, "grid_nodes_per_plane": info.mgrid, "planes": p.mzetamax,
-                       "decomposition": f"{world} toroidal domain(s)", "bin_every": p.bin_every,
-                       "l2": "inputs larger than L2 (particle SoA %.1f GB/GPU)" % (n_local * 11 * 8 / 1e9)},
+                       "decomposition": f"{ntor} toroidal x {args.nradial} radial x {args.npartdom} particle",
+                       "micell": p.micell, "bin_every": p.bin_every,
+                       "l2": "inputs larger than L2 (particle SoA %.1f GB/GPU)"
+                             % (n_local * 11 * (8 if args.precision == 64 else 4) / 1e9)},
             "value_charge_push_shift": n_total * args.steps / (cps_ms * 1e-3) if cps_ms else None,
             "phase_ms_per_step": {k[:-3]: tm[k] / args.steps for k in tm if k.endswith("_ms")},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": r.get("achieved_gbs"), "peak": hbm,
@@ -320,6 +327,11 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    # non-default decompositions / classes (the driver's runs use the defaults)
+    ap.add_argument("--nradial", type=int, default=1)
+    ap.add_argument("--npartdom", type=int, default=1)
+    ap.add_argument("--micell", type=int, default=None)
+    ap.add_argument("--precision", type=int, default=64, choices=[64, 32])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

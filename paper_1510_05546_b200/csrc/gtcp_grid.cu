@@ -370,7 +370,8 @@ void launch_add_zonal2(const Geo& g, const double* phi00, const double* phi, dou
 
 // F-5 field on planes 0..P from phi H array (planes -1..P+1 filled) into the
 // gather layout gf[interval][node][plane-of-interval][3].
-__global__ void k_field(Geo g, const double* __restrict__ phiH, double* __restrict__ gf) {
+template <class FT>
+__global__ void k_field(Geo g, const double* __restrict__ phiH, FT* __restrict__ gf) {
     long long total = (long long)(g.P + 1) * g.mgrid;
     const double inv2dz = 1.0 / (2.0 * g.dzeta);
     GRID_LOOP(e, total) {
@@ -395,28 +396,31 @@ __global__ void k_field(Geo g, const double* __restrict__ phiH, double* __restri
         double gt = (pl[ig + jp] - pl[ig + jm]) / (2.0 * dth);
         double gp = (pl[g.mgrid + ig + j] - pl[-(long long)g.mgrid + ig + j]) * inv2dz;
         if (k < g.P) {
-            double* o = gf + ((long long)k * g.mgrid + node) * 6;
-            o[0] = gr; o[1] = gt; o[2] = gp;
+            FT* o = gf + ((long long)k * g.mgrid + node) * 6;
+            o[0] = (FT)gr; o[1] = (FT)gt; o[2] = (FT)gp;
         }
         if (k > 0) {
-            double* o = gf + ((long long)(k - 1) * g.mgrid + node) * 6 + 3;
-            o[0] = gr; o[1] = gt; o[2] = gp;
+            FT* o = gf + ((long long)(k - 1) * g.mgrid + node) * 6 + 3;
+            o[0] = (FT)gr; o[1] = (FT)gt; o[2] = (FT)gp;
         }
     }
 }
 
 void launch_field(const Geo& g, const double* phi, double* gfield, cudaStream_t st) {
-    k_field<<<blocks_for((long long)(g.P + 1) * g.mgrid), 256, 0, st>>>(g, phi, gfield);
+    // precision 32: the gather field is stored in fp32 next to the fp32 particle state
+    if (g.prec32) k_field<float><<<blocks_for((long long)(g.P + 1) * g.mgrid), 256, 0, st>>>(g, phi, (float*)gfield);
+    else k_field<double><<<blocks_for((long long)(g.P + 1) * g.mgrid), 256, 0, st>>>(g, phi, gfield);
     g_launches++;
 }
 
 // gather layout -> (P+1) x mgrid x 3 plane-major
-__global__ void k_gfield_export(Geo g, const double* __restrict__ gf, double* __restrict__ out) {
+template <class FT>
+__global__ void k_gfield_export(Geo g, const FT* __restrict__ gf, double* __restrict__ out) {
     long long total = (long long)(g.P + 1) * g.mgrid;
     GRID_LOOP(e, total) {
         int k = (int)(e / g.mgrid), node = (int)(e % g.mgrid);
-        const double* s = (k < g.P) ? gf + ((long long)k * g.mgrid + node) * 6
-                                    : gf + ((long long)(k - 1) * g.mgrid + node) * 6 + 3;
+        const FT* s = (k < g.P) ? gf + ((long long)k * g.mgrid + node) * 6
+                                : gf + ((long long)(k - 1) * g.mgrid + node) * 6 + 3;
         out[e * 3 + 0] = s[0];
         out[e * 3 + 1] = s[1];
         out[e * 3 + 2] = s[2];
@@ -424,24 +428,29 @@ __global__ void k_gfield_export(Geo g, const double* __restrict__ gf, double* __
 }
 
 void launch_gfield_export(const Geo& g, const double* gfield, double* out, cudaStream_t st) {
-    k_gfield_export<<<blocks_for((long long)(g.P + 1) * g.mgrid), 256, 0, st>>>(g, gfield, out);
+    if (g.prec32)
+        k_gfield_export<float><<<blocks_for((long long)(g.P + 1) * g.mgrid), 256, 0, st>>>(g, (const float*)gfield, out);
+    else k_gfield_export<double><<<blocks_for((long long)(g.P + 1) * g.mgrid), 256, 0, st>>>(g, gfield, out);
     g_launches++;
 }
 
-__global__ void k_gfield_import(Geo g, const double* __restrict__ in, double* __restrict__ gf) {
+template <class FT>
+__global__ void k_gfield_import(Geo g, const double* __restrict__ in, FT* __restrict__ gf) {
     long long total = (long long)(g.P + 1) * g.mgrid;
     GRID_LOOP(e, total) {
         int k = (int)(e / g.mgrid), node = (int)(e % g.mgrid);
         for (int c = 0; c < 3; c++) {
             double v = in[e * 3 + c];
-            if (k < g.P) gf[((long long)k * g.mgrid + node) * 6 + c] = v;
-            if (k > 0) gf[((long long)(k - 1) * g.mgrid + node) * 6 + 3 + c] = v;
+            if (k < g.P) gf[((long long)k * g.mgrid + node) * 6 + c] = (FT)v;
+            if (k > 0) gf[((long long)(k - 1) * g.mgrid + node) * 6 + 3 + c] = (FT)v;
         }
     }
 }
 
 void launch_gfield_import(const Geo& g, const double* in, double* gfield, cudaStream_t st) {
-    k_gfield_import<<<blocks_for((long long)(g.P + 1) * g.mgrid), 256, 0, st>>>(g, in, gfield);
+    if (g.prec32)
+        k_gfield_import<float><<<blocks_for((long long)(g.P + 1) * g.mgrid), 256, 0, st>>>(g, in, (float*)gfield);
+    else k_gfield_import<double><<<blocks_for((long long)(g.P + 1) * g.mgrid), 256, 0, st>>>(g, in, gfield);
     g_launches++;
 }
 

@@ -17,6 +17,7 @@
 // Eqs. 2-8; bin P:317-318.  Readings: SURVEY §8(c).
 #include <cooperative_groups.h>
 #include <cstdlib>
+#include <type_traits>
 
 #include "gtcp_internal.cuh"
 
@@ -737,7 +738,9 @@ __device__ __forceinline__ double warp_max(double v) {
 // One RK2 stage of one particle (U-1..U-8): returns the new state X[5] from
 // the source state (psi, theta, zeta, rho_par, w), mu and the base state.
 // Counts reflections / plane clamps into the caller's registers.
-template <int GU = 8>
+// FT: storage type of the gather field (double; float with the fp32 particle
+// state of precision 32), arithmetic always fp64
+template <int GU = 8, class FT = double>
 __device__ __forceinline__ void push_one(const Geo& g, const RingTab* __restrict__ rt, double psi, double theta,
                                          double zeta, double rho_par, double w, double mu, const double* base,
                                          double h, const double* __restrict__ gf, double* X, long long& refl,
@@ -792,12 +795,13 @@ __device__ __forceinline__ void push_one(const Geo& g, const RingTab* __restrict
     // phase 2: 8 x 96 contiguous bytes of the interval-interleaved field; each
     // bounding plane accumulated separately, plane weights and 1/4 applied once
     double r0 = 0.0, t0 = 0.0, p0 = 0.0, r1 = 0.0, t1 = 0.0, p1 = 0.0;
-    const double* gk = gf + (long long)k * g.mgrid * 6;
+    using V2 = typename std::conditional<std::is_same<FT, float>::value, float2, double2>::type;
+    const FT* gk = reinterpret_cast<const FT*>(gf) + (long long)k * g.mgrid * 6;
 #pragma unroll GU
     for (int q = 0; q < 8; q++) {
-        const double2* qq = reinterpret_cast<const double2*>(gk + (long long)node[q] * 6);
-        const double2 v0 = qq[0], v1 = qq[1], v2 = qq[2];
-        const double2 v3 = qq[3], v4 = qq[4], v5 = qq[5];
+        const V2* qq = reinterpret_cast<const V2*>(gk + (long long)node[q] * 6);
+        const V2 v0 = qq[0], v1 = qq[1], v2 = qq[2];
+        const V2 v3 = qq[3], v4 = qq[4], v5 = qq[5];
         const double a0 = wa[q], a1 = wb[q];
         // node j: (v0.x v0.y v1.x) plane k, (v1.y v2.x v2.y) plane k+1; node j+1 likewise in v3..v5
         r0 = fma(a0, v0.x, fma(a1, v3.x, r0));
@@ -894,7 +898,7 @@ __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long lon
         double base[5], X[5];
 #pragma unroll
         for (int d = 0; d < 5; d++) base[d] = ld(pp.base[d]);
-        push_one<GU>(g, rt_dyn, ld(pp.src[0]), ld(pp.src[1]), ld(pp.src[2]), ld(pp.src[3]), ld(pp.src[4]), ld(pp.mu),
+        push_one<GU, R>(g, rt_dyn, ld(pp.src[0]), ld(pp.src[1]), ld(pp.src[2]), ld(pp.src[3]), ld(pp.src[4]), ld(pp.mu),
                  base, h, gf, X, refl, clamps);
         // one test: a NaN or Inf in any component survives the product with 0
         if (!isfinite((X[0] + X[1] + X[2] + X[3]) * 0.0 + X[4])) nonfinite = 1;
