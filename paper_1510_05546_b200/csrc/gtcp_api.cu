@@ -749,9 +749,24 @@ extern "C" gtcp_status gtcp_poisson_smooth(gtcp_ctx c) {
     launch_ring_sum(g, c->dnH, c->ringsum, c->st);
     if (c->prm.ntoroidal > 1) NC(ncclAllReduce(c->ringsum, c->ringsum, g.mpsi + 1, ncclDouble, ncclSum, c->tor, c->st));
     launch_jacobi_init(g, c->dnH, c->ringsum, c->rhs, c->jphi, c->st);
+    // the Poisson equation is 2-D per plane: the ranks of a section (radial
+    // windows and particle replicas of one toroidal domain hold the same grid)
+    // split the planes of the Jacobi sweeps and then share the result
+    const int S = c->prm.nradial * c->prm.npartdom, s_me = c->rank_r * c->prm.npartdom + c->rank_p;
+    auto kb = [&](int r) { return (int)((long long)r * c->P / S); };
     for (int it = 0; it < c->prm.poisson_iters; it++) {
-        launch_gyro(g, c->d_pois, c->jphi, c->g1, c->st);
-        launch_gyro_jacobi(g, c->d_pois, c->g1, c->rhs, c->jphi, c->prm.jacobi_omega, c->st);
+        launch_gyro(g, c->d_pois, c->jphi, c->g1, kb(s_me), kb(s_me + 1) - kb(s_me), c->st);
+        launch_gyro_jacobi(g, c->d_pois, c->g1, c->rhs, c->jphi, c->prm.jacobi_omega, kb(s_me),
+                           kb(s_me + 1) - kb(s_me), c->st);
+    }
+    if (S > 1) {
+        NC(ncclGroupStart());
+        for (int r = 0; r < S; r++) {
+            double* bp = c->jphi + (long long)kb(r) * c->mgrid;
+            const size_t cnt = (size_t)(kb(r + 1) - kb(r)) * c->mgrid;
+            if (cnt) NC(ncclBroadcast(bp, bp, cnt, ncclDouble, r, c->sect, c->st));
+        }
+        NC(ncclGroupEnd());
     }
     launch_zonal(g, c->ringsum, c->phi00, c->st);
     launch_add_zonal2(g, c->phi00, c->jphi, c->phiH, c->st);

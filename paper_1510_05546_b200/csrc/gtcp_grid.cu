@@ -272,10 +272,10 @@ __device__ __forceinline__ double gyro_value_tab(const PoisRing* __restrict__ R,
     return 0.25 * v;
 }
 
-// F-1 on every owned plane (plain arrays); grid (nodes, planes)
+// F-1 on planes kbeg.. of the plain arrays; grid (nodes, planes)
 __global__ void k_gyro(Geo g, const PoisRing* __restrict__ pr, const double* __restrict__ in,
-                       double* __restrict__ out) {
-    const int k = blockIdx.y;
+                       double* __restrict__ out, int kbeg) {
+    const int k = kbeg + blockIdx.y;
     const int node = blockIdx.x * blockDim.x + threadIdx.x;
     if (node >= g.mgrid) return;
     const long long e = (long long)k * g.mgrid + node;
@@ -286,18 +286,22 @@ __global__ void k_gyro(Geo g, const PoisRing* __restrict__ pr, const double* __r
     out[e] = gyro_value_tab(R, in + (long long)k * g.mgrid, j, (double)(g.k0 + k) * g.dzeta);
 }
 
-static dim3 grid_nodes_planes(const Geo& g) { return dim3((unsigned)((g.mgrid + 255) / 256), (unsigned)g.P); }
+static dim3 grid_nodes_planes(const Geo& g, int kcount) {
+    return dim3((unsigned)((g.mgrid + 255) / 256), (unsigned)kcount);
+}
 
-void launch_gyro(const Geo& g, const PoisRing* pr, const double* in, double* out, cudaStream_t st) {
-    k_gyro<<<grid_nodes_planes(g), 256, 0, st>>>(g, pr, in, out);
+void launch_gyro(const Geo& g, const PoisRing* pr, const double* in, double* out, int kbeg, int kcount,
+                 cudaStream_t st) {
+    if (kcount <= 0) return;
+    k_gyro<<<grid_nodes_planes(g, kcount), 256, 0, st>>>(g, pr, in, out, kbeg);
     g_launches++;
 }
 
 // second G application fused with the Jacobi update (F-2):
 // phi <- (1-omega) phi + omega (rhs + G(g1)) / (1 + 1/tau), phi = 0 on rings 0, mpsi
 __global__ void k_gyro_jacobi(Geo g, const PoisRing* __restrict__ pr, const double* __restrict__ g1,
-                              const double* __restrict__ rhs, double* __restrict__ phi, double omega) {
-    const int k = blockIdx.y;
+                              const double* __restrict__ rhs, double* __restrict__ phi, double omega, int kbeg) {
+    const int k = kbeg + blockIdx.y;
     const int node = blockIdx.x * blockDim.x + threadIdx.x;
     if (node >= g.mgrid) return;
     const long long e = (long long)k * g.mgrid + node;
@@ -312,8 +316,9 @@ __global__ void k_gyro_jacobi(Geo g, const PoisRing* __restrict__ pr, const doub
 }
 
 void launch_gyro_jacobi(const Geo& g, const PoisRing* pr, const double* g1, const double* rhs, double* phi,
-                        double omega, cudaStream_t st) {
-    k_gyro_jacobi<<<grid_nodes_planes(g), 256, 0, st>>>(g, pr, g1, rhs, phi, omega);
+                        double omega, int kbeg, int kcount, cudaStream_t st) {
+    if (kcount <= 0) return;
+    k_gyro_jacobi<<<grid_nodes_planes(g, kcount), 256, 0, st>>>(g, pr, g1, rhs, phi, omega, kbeg);
     g_launches++;
 }
 

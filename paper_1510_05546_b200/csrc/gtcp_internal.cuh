@@ -129,9 +129,10 @@ void launch_smooth_par(const Geo& g, const double* in, double* out, cudaStream_t
 void launch_ring_sum(const Geo& g, const double* f, double* ringsum, cudaStream_t st);
 void launch_jacobi_init(const Geo& g, const double* dn, const double* ringsum, double* rhs, double* phi,
                         cudaStream_t st);
-void launch_gyro(const Geo& g, const PoisRing* pr, const double* in, double* out, cudaStream_t st);
+void launch_gyro(const Geo& g, const PoisRing* pr, const double* in, double* out, int kbeg, int kcount,
+                 cudaStream_t st);
 void launch_gyro_jacobi(const Geo& g, const PoisRing* pr, const double* g1, const double* rhs, double* phi,
-                        double omega, cudaStream_t st);
+                        double omega, int kbeg, int kcount, cudaStream_t st);
 void launch_zonal(const Geo& g, const double* ringsum, double* phi00, cudaStream_t st);
 void launch_add_zonal2(const Geo& g, const double* phi00, const double* phi, double* phiH, cudaStream_t st);
 void launch_field(const Geo& g, const double* phi, double* gfield, cudaStream_t st);
