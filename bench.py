@@ -209,7 +209,14 @@ def run_gpu(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     barrier()
+    sync_t = torch.zeros(1, device="cuda")
     with ClockSampler(local) as clk:
+        if dist:
+            # device-side start line: a collective on the context stream right
+            # before the start event, so host launch skew after the barrier is
+            # not counted as step time on the ranks that wait for the others
+            with torch.cuda.stream(stream):
+                dist.all_reduce(sync_t)
         ev0.record(stream)
         for _ in range(args.steps):
             ctx.step(1)
