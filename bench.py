@@ -129,11 +129,27 @@ def cpu_baseline(size: str, n_sample: int, steps: int = 1):
     return n_sample * steps / dt, dt
 
 
+def workload_config(size: str, n_gpus: int, args) -> dict:
+    """The workload both arms report (same keys and strings): class, grid,
+    marker count, decomposition."""
+    import synth
+    over = {"micell": args.micell} if args.micell else {}
+    cfg = synth.config(size, **over)
+    import oracle
+    g = oracle.geometry(oracle.make_params(cfg))
+    ntor = max(1, n_gpus // (args.nradial * args.npartdom))
+    return {"workload": f"GTC-P class {size}: mpsi={cfg['mpsi']} mthetamax={cfg['mthetamax']} "
+                        f"mzetamax={cfg['mzetamax']} micell={cfg['micell']}",
+            "particles": int(cfg["micell"] * (g.mgrid - cfg["mpsi"]) * cfg["mzetamax"]),
+            "grid_nodes_per_plane": int(g.mgrid), "planes": cfg["mzetamax"],
+            "decomposition": f"{ntor} toroidal x {args.nradial} radial x {args.npartdom} particle"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    size = args.size or "A"
+    size = args.size or ("A" if args.gpus == 1 else "B")  # the same workload as the b200 arm
     n_sample = args.ref_sample
     import oracle
     oracle.build()
@@ -147,9 +163,9 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / len(vals),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"GTC-P class {size} grid, oracle on a {n_sample}-marker sample per step",
-                   "size": size},
+        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": workload_config(size, args.gpus, args),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
                          "sample": f"{n_sample} markers of class {size} on its full grid, charge+push+shift, "
                                    f"fixed prescribed field, {len(vals)} steps"},
@@ -301,13 +317,9 @@ def run_gpu(args):
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "state_storage": "f64" if args.precision == 64 else "f32 (arithmetic f64)",
             "data": "synthetic",
-            "config": {"workload": f"GTC-P class {size}: mpsi={p.mpsi} mthetamax={p.mthetamax} "
-                                   f"mzetamax={p.mzetamax} micell={p.micell}",
-                       "particles": n_total, "grid_nodes_per_plane": info.mgrid, "planes": p.mzetamax,
-                       "decomposition": f"{ntor} toroidal x {args.nradial} radial x {args.npartdom} particle",
-                       "micell": p.micell, "bin_every": p.bin_every,
-                       "l2": "inputs larger than L2 (particle SoA %.1f GB/GPU)"
-                             % (n_local * 11 * (8 if args.precision == 64 else 4) / 1e9)},
+            "config": dict(workload_config(size, world, args), micell=p.micell, bin_every=p.bin_every,
+                           l2="inputs larger than L2 (particle SoA %.1f GB/GPU)"
+                              % (n_local * 11 * (8 if args.precision == 64 else 4) / 1e9)),
             "value_charge_push_shift": n_total * args.steps / (cps_ms * 1e-3) if cps_ms else None,
             "phase_ms_per_step": {k[:-3]: tm[k] / args.steps for k in tm if k.endswith("_ms")},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": r.get("achieved_gbs"), "peak": hbm,
