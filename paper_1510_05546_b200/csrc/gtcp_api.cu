@@ -1107,13 +1107,11 @@ extern "C" gtcp_status gtcp_get_grid(gtcp_ctx c, int which, int64_t cap, double*
         }
         case GTCP_GRID_GRADPHI: {
             if (cap < planes * mg * 3) return set_err(c, GTCP_ECAPACITY, "get_grid: cap");
-            double* tmp = c->tmpH;  // (P+3) mg >= 3 (P+1) mg only if P >= 0... use dnH+tmpH contiguous? allocate
-            double* buf;
+            double* buf;  // stream-ordered scratch for the plane-major export
             CU(cudaMallocAsync((void**)&buf, planes * mg * 3 * sizeof(double), c->st));
             launch_gfield_export(c->geo, c->gfield, buf, c->st);
             CU(cudaMemcpyAsync(host, buf, planes * mg * 3 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
             CU(cudaFreeAsync(buf, c->st));
-            (void)tmp;
             break;
         }
         case GTCP_GRID_MARKER: {

@@ -490,12 +490,23 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
                 const double x = __dmul_rn(__dsub_rn(rl, g.a0), g.inv_dr);
                 const int ir = min(max((int)floor(x), 0), g.mpsi - 1);
                 const double wp1 = __dsub_rn(x, (double)ir);
+                // both rings' table entries and window rows are fetched before
+                // any use, so the shared-memory latency overlaps the arithmetic
+                int qcs[2];
+                RingT rts[2];
+                int2 rows[2][2];
+#pragma unroll
+                for (int mq = 0; mq < 2; mq++) {
+                    const int q = ir + (mq ^ b2) - m_lo;
+                    qcs[mq] = (unsigned)q < (unsigned)nr ? q : nr;
+                    rts[mq] = RT[qcs[mq]];
+                    rows[mq][0] = rowA[qcs[mq]];
+                    rows[mq][1] = rowB[qcs[mq]];
+                }
 #pragma unroll
                 for (int mq = 0; mq < 2; mq++) {
                     const int mm = mq ^ b2;  // lane-rotated ring choice
-                    const int q = ir + mm - m_lo;
-                    const int qc = (unsigned)q < (unsigned)nr ? q : nr;
-                    const RingT rt = RT[qc];
+                    const RingT rt = rts[mq];
                     double sl = __dmul_rn(__fma_rn(-zeta, rt.qt, tl2), kInvTwoPi);
                     sl = __dsub_rn(sl, floor(sl));
                     sl = __dmul_rn(sl, rt.mtd);
@@ -512,7 +523,7 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
                     const int ja = b4 ? j1 : j, jb = b4 ? j : j1;
 #pragma unroll
                     for (int kq = 0; kq < 2; kq++) {
-                        const int2 row = (kq ? rowB : rowA)[qc];
+                        const int2 row = rows[mq][kq];
                         const unsigned da = wrap_diff(ja, row.x, rt.mt), db = wrap_diff(jb, row.x, rt.mt);
                         bad = max(bad, (int)max(da, db) - rt.W);
                         const int oa = row.y + 4 * (int)min(da, (unsigned)rt.W);
