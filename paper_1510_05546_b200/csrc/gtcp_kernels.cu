@@ -111,11 +111,14 @@ __device__ __forceinline__ void gyro_stencil(const Geo& g, double r, double thet
 // per-particle gyroradius inputs with explicit roundings (shared by all kernels)
 __device__ __forceinline__ void gyro_radius(const Geo& g, double psi, double ct, double mu, double* r, double* invB,
                                             double* rho, double* inv_r) {
+    // one reciprocal square root per radicand: sqrt(x) = x * rsqrt(x) (within
+    // an ulp of sqrt; psi >= a0^2/2 > 0 always, the gyro radicand may be 0)
     const double two_psi = __dmul_rn(2.0, psi);
-    *r = sqrt(two_psi);
     *inv_r = rsqrt(two_psi);
+    *r = __dmul_rn(two_psi, *inv_r);
     *invB = __fma_rn(__dmul_rn(*r, g.inv_R0), ct, 1.0);
-    *rho = __dmul_rn(sqrt(__dmul_rn(__dmul_rn(2.0, mu), *invB)), g.inv_omega0);
+    const double rad = __dmul_rn(__dmul_rn(2.0, mu), *invB);
+    *rho = rad > 0.0 ? __dmul_rn(__dmul_rn(rad, rsqrt(rad)), g.inv_omega0) : 0.0;
 }
 
 // Global fixed-point grid index of canonical node (kk, m, j), j < mt.  On a
