@@ -99,6 +99,9 @@ typedef struct {
     double vcut;            /* velocity cutoff 5 v_th (L-3)                    */
     double capacity_factor; /* particle-array headroom for shift arrivals      */
     uint64_t seed;          /* gtcp_load Philox key                            */
+    int32_t field_f32;      /* store the gather field in fp32 with an fp64 state (experiment;
+                             * precision 32 always does); 0 */
+    int32_t reserved2;
 } gtcp_params;
 
 /* Per-context sizes and counters.  Host copy; filled by gtcp_info / gtcp_stats. */

@@ -39,7 +39,7 @@ class Params(C.Structure):
         ("a0", C.c_double), ("a1", C.c_double), ("R0", C.c_double), ("omega0", C.c_double),
         ("q0", C.c_double), ("q2", C.c_double), ("rln", C.c_double), ("rlt", C.c_double),
         ("tau", C.c_double), ("dt", C.c_double), ("jacobi_omega", C.c_double), ("w_init_amp", C.c_double),
-        ("vcut", C.c_double), ("capacity_factor", C.c_double), ("seed", C.c_uint64),
+        ("vcut", C.c_double), ("capacity_factor", C.c_double), ("seed", C.c_uint64), ("field_f32", C.c_int32), ("reserved2", C.c_int32),
     ]
 
     def as_dict(self):

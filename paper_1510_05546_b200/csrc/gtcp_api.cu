@@ -325,6 +325,7 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     g.mpsi = M; g.mzetamax = p->mzetamax; g.P = P; g.k0 = c->k0; g.ntor = p->ntoroidal; g.rank_t = c->rank_t;
     g.mgrid = mg; g.paranl = p->paranl; g.drifts = p->drifts;
     g.prec32 = (p->precision == 32);
+    g.f32field = g.prec32 || p->field_f32 != 0;
     gtcp::g_prec32 = g.prec32;
     const size_t es = g.prec32 ? sizeof(float) : sizeof(double);  // particle element size
     g.a0 = p->a0; g.a1 = p->a1; g.dr = (p->a1 - p->a0) / M; g.inv_dr = 1.0 / g.dr;

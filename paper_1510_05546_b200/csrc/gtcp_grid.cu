@@ -413,7 +413,7 @@ __global__ void k_field(Geo g, const double* __restrict__ phiH, FT* __restrict__
 
 void launch_field(const Geo& g, const double* phi, double* gfield, cudaStream_t st) {
     // precision 32: the gather field is stored in fp32 next to the fp32 particle state
-    if (g.prec32) k_field<float><<<blocks_for((long long)(g.P + 1) * g.mgrid), 256, 0, st>>>(g, phi, (float*)gfield);
+    if (g.f32field) k_field<float><<<blocks_for((long long)(g.P + 1) * g.mgrid), 256, 0, st>>>(g, phi, (float*)gfield);
     else k_field<double><<<blocks_for((long long)(g.P + 1) * g.mgrid), 256, 0, st>>>(g, phi, gfield);
     g_launches++;
 }
@@ -433,7 +433,7 @@ __global__ void k_gfield_export(Geo g, const FT* __restrict__ gf, double* __rest
 }
 
 void launch_gfield_export(const Geo& g, const double* gfield, double* out, cudaStream_t st) {
-    if (g.prec32)
+    if (g.f32field)
         k_gfield_export<float><<<blocks_for((long long)(g.P + 1) * g.mgrid), 256, 0, st>>>(g, (const float*)gfield, out);
     else k_gfield_export<double><<<blocks_for((long long)(g.P + 1) * g.mgrid), 256, 0, st>>>(g, gfield, out);
     g_launches++;
@@ -453,7 +453,7 @@ __global__ void k_gfield_import(Geo g, const double* __restrict__ in, FT* __rest
 }
 
 void launch_gfield_import(const Geo& g, const double* in, double* gfield, cudaStream_t st) {
-    if (g.prec32)
+    if (g.f32field)
         k_gfield_import<float><<<blocks_for((long long)(g.P + 1) * g.mgrid), 256, 0, st>>>(g, in, (float*)gfield);
     else k_gfield_import<double><<<blocks_for((long long)(g.P + 1) * g.mgrid), 256, 0, st>>>(g, in, gfield);
     g_launches++;

@@ -23,6 +23,7 @@ struct Geo {
     int mgrid;                     // nodes per plane incl. duplicates (< 2^31)
     int paranl, drifts;
     int prec32;                    // particle store in fp32 (arithmetic stays fp64)
+    int f32field;                  // gather field stored in fp32 (precision 32, or field_f32)
     double a0, a1, dr, inv_dr, R0, inv_R0, omega0, q0, q2, rln, rlt, tau, dt;
     double cz;                     // mzetamax / (2 pi), rounded once (Q-2, H-1)
     double psi_lo, psi_hi;         // a0^2/2, a1^2/2 padded inwards: psi strictly inside needs no reflection test

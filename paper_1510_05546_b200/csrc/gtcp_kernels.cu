@@ -897,7 +897,7 @@ __device__ __forceinline__ void push_epilogue(DevCounters* dc, double wmax, long
     if (nonfinite) dc->nonfinite = 1;
 }
 
-template <int MINB, bool CS, int GU = 8, class R = double>
+template <int MINB, bool CS, int GU = 8, class R = double, class FT = R>
 __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long long n, double h,
                                              const double* __restrict__ gf, DevCounters* dc) {
     extern __shared__ RingTab rt_dyn[];
@@ -912,7 +912,7 @@ __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long lon
         double base[5], X[5];
 #pragma unroll
         for (int d = 0; d < 5; d++) base[d] = ld(pp.base[d]);
-        push_one<GU, R>(g, rt_dyn, ld(pp.src[0]), ld(pp.src[1]), ld(pp.src[2]), ld(pp.src[3]), ld(pp.src[4]), ld(pp.mu),
+        push_one<GU, FT>(g, rt_dyn, ld(pp.src[0]), ld(pp.src[1]), ld(pp.src[2]), ld(pp.src[3]), ld(pp.src[4]), ld(pp.mu),
                  base, h, gf, X, refl, clamps);
         // one test: a NaN or Inf in any component survives the product with 0
         if (!isfinite((X[0] + X[1] + X[2] + X[3]) * 0.0 + X[4])) nonfinite = 1;
@@ -958,6 +958,7 @@ void launch_push3(const Geo& g, const double* const src[5], const double* const 
     int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
     size_t smr = (g.mpsi + 1) * sizeof(RingTab);
     if (g.prec32) k_push<2, true, 8, float><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
+    else if (g.f32field) k_push<2, true, 8, double, float><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
     else k_push<2, true, 8, double><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
     g_launches++;
 }

@@ -142,3 +142,23 @@ def test_zero_weights_give_zero_charge(G, Tcfg):
     ctx.set_particles(parts)
     ctx.charge()
     assert not np.any(ctx.get_grid(G.GRID_CHARGE))
+
+
+def test_fp32_gather_field_with_fp64_state(G, orc, Tcfg):
+    """field_f32 (experiment): the gather field stored in fp32 next to an fp64
+    state.  Its rounding (2^-24 relative) moves the pushed state far less than
+    the P-0 tolerance."""
+    cfg, p, g = Tcfg
+    parts = synth.load_particles(cfg, 12100, seed=5, w_amp=0.1)
+    gp = _smooth_field(orc, p, g)
+    ctx = ctx_for(G, "T", field_f32=1)
+    ctx.set_particles(parts)
+    ctx.set_grid(G.GRID_GRADPHI, gp)
+    Xa = {k: parts[k].copy() for k in orc.ATTRS}
+    Xb = {k: parts[k].copy() for k in orc.ATTRS}
+    ctx.push(1)
+    ctx.push(2)
+    orc.push(p, 1, Xa, Xb, parts["mu"], gp)
+    orc.push(p, 2, Xa, Xb, parts["mu"], gp)
+    got = ctx.get_particles()
+    assert_particles_close({**{k: got[k] for k in orc.ATTRS}, "id": got["id"]}, {**Xa, "id": parts["id"]})

@@ -19,6 +19,7 @@ ap.add_argument("--micell", type=int, default=None)
 ap.add_argument("--bin-mu", type=int, default=None)
 ap.add_argument("--mzetamax", type=int, default=None)
 ap.add_argument("--precision", type=int, default=64)
+ap.add_argument("--field-f32", type=int, default=0)
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -32,6 +33,7 @@ if a.bin_mu:
 if a.mzetamax:
     over["mzetamax"] = a.mzetamax
 over["precision"] = a.precision
+over["field_f32"] = a.field_f32
 stream = torch.cuda.Stream()
 ctx = G.Context(G.gtcp_default_params(a.size, bin_every=a.bin_every, **over), stream=stream.cuda_stream)
 ctx.set_charge_mode(a.charge_mode)
