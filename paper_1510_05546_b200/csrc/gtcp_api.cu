@@ -391,7 +391,7 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     }
     double headroom = nranks > 1 ? 0.10 : 0.0;
     c->cap = (long long)std::ceil(n_load * (p->capacity_factor + headroom)) + 1024;
-    c->cap = (c->cap + 255) / 256 * 256;  // TMA-staged kernels copy whole 16-byte granules of 256-particle chunks
+    c->cap = (c->cap + 255) / 256 * 256;  // whole 256-particle blocks (and 16-byte aligned class-byte loads)
     // particle arrays hold `es`-byte reals (fp64 or fp32 state); typed double* for plumbing only
     auto palloc = [&](double** ptr, long long count) { return cudaMalloc((void**)ptr, std::max<long long>(count, 1) * es); };
     for (int d = 0; d < 5; d++) {
