@@ -15,7 +15,6 @@
 
 namespace gtcp {
 
-static constexpr int kShiftBlock = 1024;
 
 __device__ __forceinline__ int shift_plane(const Geo& g, double zeta) {
     double tg = __dmul_rn(zeta, g.cz);
@@ -23,40 +22,9 @@ __device__ __forceinline__ int shift_plane(const Geo& g, double zeta) {
     return min(max(k, 0), g.mzetamax - 1);
 }
 
-// Every kernel below walks a chunk of kChunk consecutive particles per block:
-// warp w owns the kSub = kChunk/32 particles [base + w*kSub, base + (w+1)*kSub)
-// in kIt coalesced steps of 32, keeps its per-step ballot masks in registers,
-// and a single block-level scan of the 32 warp totals gives every warp its
-// output offset (one barrier per chunk).
-static constexpr int kChunk = 16 * kShiftBlock;
-static constexpr int kSub = kChunk / 32;  // particles per warp
-static constexpr int kIt = kSub / 32;     // steps per warp
-
-// exclusive scan of one value per warp over the block; returns this warp's
-// offset and the block total (all threads call it)
-__device__ __forceinline__ unsigned warp_offsets(unsigned v, unsigned* sw, unsigned* total) {
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) sw[w] = v;
-    __syncthreads();
-    if (w == 0) {
-        unsigned x = sw[lane], y = x;
-        for (int o = 1; o < 32; o <<= 1) {
-            unsigned t = __shfl_up_sync(0xffffffffu, y, o);
-            if (lane >= o) y += t;
-        }
-        sw[lane] = y - x;
-        if (lane == 31) sw[32] = y;
-    }
-    __syncthreads();
-    unsigned off = sw[w];
-    *total = sw[32];
-    __syncthreads();
-    return off;
-}
-
-__device__ __forceinline__ long long warp_p(long long base, int it) {
-    return base + (long long)(threadIdx.x >> 5) * kSub + it * 32 + (threadIdx.x & 31);
-}
+// Every kernel below works on chunks of kChunk consecutive particles (the
+// granularity of the per-chunk mover / hole / filler counts and their scans).
+static constexpr int kChunk = 16384;  // == 1 << kShiftChunkLog2 of the fused classification in k_push
 
 // The list/count kernels: one block of kLT threads per chunk; thread t owns
 // particles [base + kPer t, base + kPer (t+1)) of its chunk (thread order =
@@ -168,35 +136,33 @@ __device__ __forceinline__ int radial_domain(const Geo& g, double psi) {
 
 // classify: cls[p] in {0 keep, 1 left, 2 right}; per-chunk mover counts.
 // mode 0: toroidal (periodic ring, the shorter way round); mode 1: radial
-// (inner = left, outer = right, not periodic)
+// (inner = left, outer = right, not periodic).  One kLT-thread block per
+// chunk; each warp walks a contiguous 2048-marker slice in coalesced steps.
 template <class R>
-__global__ void __launch_bounds__(kShiftBlock) k_shift_classify(Geo g, const double* __restrict__ zeta,
-                                                                const double* __restrict__ psi, int mode, long long n,
-                                                                unsigned char* __restrict__ cls,
-                                                                unsigned* __restrict__ cntL,
-                                                                unsigned* __restrict__ cntR) {
+__global__ void __launch_bounds__(kLT) k_shift_classify(Geo g, const double* __restrict__ zeta,
+                                                        const double* __restrict__ psi, int mode, long long n,
+                                                        unsigned char* __restrict__ cls,
+                                                        unsigned* __restrict__ cntL,
+                                                        unsigned* __restrict__ cntR) {
     __shared__ unsigned sw[33];
     const long long base = (long long)blockIdx.x * kChunk;
-    const double* key = mode ? psi : zeta;
-    double z[kIt];
-#pragma unroll
-    for (int it = 0; it < kIt; it++) {
-        long long p = warp_p(base, it);
-        z[it] = (p < n) ? (double)__ldcs(reinterpret_cast<const R*>(key) + p) : 0.0;
-    }
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int kWarps = kLT / 32, kSlice = kChunk / kWarps;
+    const R* key = reinterpret_cast<const R*>(mode ? psi : zeta);
     unsigned a = 0, b = 0;
-#pragma unroll
-    for (int it = 0; it < kIt; it++) {
-        long long p = warp_p(base, it);
+#pragma unroll 8
+    for (int it = 0; it < kSlice / 32; it++) {
+        const long long p = base + (long long)w * kSlice + it * 32 + lane;
         unsigned char c = 0;
         if (p < n) {
+            const double z = (double)__ldcs(key + p);
             if (mode == 0) {
-                int d = shift_plane(g, z[it]) / g.P;
+                int d = shift_plane(g, z) / g.P;
                 int rel = d - g.rank_t;
                 if (rel < 0) rel += g.ntor;
                 if (rel != 0) c = (rel <= g.ntor / 2) ? 2 : 1;
             } else {
-                int rel = radial_domain(g, z[it]) - g.rank_r;
+                int rel = radial_domain(g, z) - g.rank_r;
                 if (rel != 0) c = (rel > 0) ? 2 : 1;
             }
             cls[p] = c;
@@ -205,8 +171,8 @@ __global__ void __launch_bounds__(kShiftBlock) k_shift_classify(Geo g, const dou
         b += __popc(__ballot_sync(0xffffffffu, c == 2));
     }
     unsigned ta, tb;
-    warp_offsets(a, sw, &ta);
-    warp_offsets(b, sw, &tb);
+    block_excl_scan(lane == 0 ? a : 0u, sw, &ta);
+    block_excl_scan(lane == 0 ? b : 0u, sw, &tb);
     if (threadIdx.x == 0) {
         cntL[blockIdx.x] = ta;
         cntR[blockIdx.x] = tb;
@@ -339,8 +305,8 @@ int shift_chunks(long long n) { return (int)std::max<long long>(1, (n + kChunk -
 void launch_shift_classify(const Geo& g, const double* zeta, const double* psi, int mode, long long n,
                            unsigned char* cls, unsigned* cntL, unsigned* cntR, cudaStream_t st) {
     int nb = shift_chunks(n);
-    if (g.prec32) k_shift_classify<float><<<nb, kShiftBlock, 0, st>>>(g, zeta, psi, mode, n, cls, cntL, cntR);
-    else k_shift_classify<double><<<nb, kShiftBlock, 0, st>>>(g, zeta, psi, mode, n, cls, cntL, cntR);
+    if (g.prec32) k_shift_classify<float><<<nb, kLT, 0, st>>>(g, zeta, psi, mode, n, cls, cntL, cntR);
+    else k_shift_classify<double><<<nb, kLT, 0, st>>>(g, zeta, psi, mode, n, cls, cntL, cntR);
     g_launches++;
 }
 
