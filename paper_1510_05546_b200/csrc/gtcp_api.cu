@@ -344,6 +344,7 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     g.rank_r = c->rank_r;
     for (int b = 0; b < 9; b++) g.rbound[b] = p->a1 + 1.0;
     for (int b = 0; b <= nrad; b++) g.rbound[b] = p->a0 + c->rad_ring[b] * g.dr;
+    for (int b = 0; b < 9; b++) g.rbound2[b] = g.rbound[b] * g.rbound[b];
     g.mtheta = c->d_mtheta; g.igrid = c->d_igrid; g.itran = c->d_itran; g.qtinv = c->d_qtinv;
     g.node_ring = c->d_node_ring;
     {

@@ -20,6 +20,7 @@ struct Geo {
     int ntor, rank_t;              // toroidal domains, this rank's toroidal index
     int nrad, rank_r;              // radial domains, this rank's radial index
     double rbound[9];              // radial domain boundaries r(b_0 = ring 0) .. r(b_nrad = ring mpsi)
+    double rbound2[9];             // their squares (fast classification away from a boundary)
     int mgrid;                     // nodes per plane incl. duplicates (< 2^31)
     int paranl, drifts;
     int prec32;                    // particle store in fp32 (arithmetic stays fp64)

@@ -128,9 +128,16 @@ __device__ __forceinline__ void emit_bits(unsigned long long m, long long p0, un
 // H-2: radial domain of a gyrocentre radius r = sqrt(2 psi) (IEEE sqrt and
 // exact comparisons against the ring radii of the window boundaries)
 __device__ __forceinline__ int radial_domain(const Geo& g, double psi) {
-    const double r = sqrt(__dmul_rn(2.0, psi));
+    // the decision is that of IEEE sqrt(2 psi) >= r_b; away from a boundary
+    // (relative margin 1e-12, far above the rounding of 2 psi and r_b^2) it is
+    // taken on 2 psi vs r_b^2 without the square root
+    const double x = __dmul_rn(2.0, psi);
     int d = 0;
-    for (int b = 1; b < g.nrad; b++) d += (r >= g.rbound[b]) ? 1 : 0;
+    for (int b = 1; b < g.nrad; b++) {
+        const double r2 = g.rbound2[b];
+        if (x > r2 * (1.0 + 1e-12)) d++;
+        else if (x >= r2 * (1.0 - 1e-12)) d += (sqrt(x) >= g.rbound[b]) ? 1 : 0;
+    }
     return d;
 }
 
