@@ -55,7 +55,7 @@ struct gtcp_ctx_s {
     int max_tiles = 0;
     int* tile_span = nullptr;  // per ring: widest cell span whose window fits smem; then per-ring tile counts
     long long n_binned = 0;  // particles [0, n_binned) are covered by tiles
-    int tile_max = 8192;  // <= 8192: bounds the smem limb sums (gtcp_kernels.cu smem_add)
+    int tile_max = 16384;  // <= 16384: bounds the smem limb sums (gtcp_kernels.cu smem_add)
     // grids
     long long* fx = nullptr;   // (P+1) * mgrid fixed-point charge
     double *rhoH = nullptr, *dnH = nullptr, *tmpH = nullptr, *phiH = nullptr;
@@ -459,6 +459,10 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     {
         const char* e = getenv("GTCP_DEPOSIT_CTAS");  // 3 (default) or 2 CTAs per SM
         c->dep_nb = (e && atoi(e) == 2) ? 2 : 3;
+    }
+    {
+        const char* e = getenv("GTCP_TILE_MAX");  // experiment: smaller deposit tiles
+        if (e) c->tile_max = std::max(256, std::min(16384, atoi(e)));
     }
     c->dep_cap_nodes = gtcp::deposit_cap_nodes(c->dep_nb);
     c->dep_smem = gtcp::deposit_tiled_smem(P, c->dep_nb);

@@ -140,11 +140,12 @@ __device__ __forceinline__ void red_i64(long long* p, long long v) {
 }
 
 // shared-memory 2-limb fixed-point add, no return value needed:
-//   v = hi * 2^17 + lo,  lo = v & (2^17 - 1) in [0, 2^17),  hi = v >> 17.
-// With |v| < 2^33 and at most 4 * kTileMax = 2^15 contributions per node per
-// tile, sum(lo) < 2^32 and |sum(hi)| < 2^31: both limbs are exact (native
-// 32-bit ATOMS.ADD, 24 lane-ops/SM/clk measured on B200).
-static constexpr int kLimbBits = 17;
+//   v = hi * 2^16 + lo,  lo = v & (2^16 - 1) in [0, 2^16),  hi = v >> 16.
+// With |v| < 2^31 and at most 4 * 16384 = 2^16 contributions per node per
+// tile (a marker's 4 gyro-points can share a node; tiles hold <= 16384
+// markers), sum(lo) < 2^32 and |sum(hi)| < 2^31: both limbs are exact
+// (native 32-bit ATOMS.ADD).
+static constexpr int kLimbBits = 16;
 __device__ __forceinline__ void smem_add(unsigned* lo, int* hi, int slot, long long v) {
     atomicAdd(lo + slot, (unsigned)v & ((1u << kLimbBits) - 1u));
     atomicAdd(hi + slot, (int)(v >> kLimbBits));
@@ -166,17 +167,17 @@ template <class R>
 __device__ __forceinline__ void stp_cs(double* a, long long p, double v) { __stcs(reinterpret_cast<R*>(a) + p, (R)v); }
 
 // ---------------------------------------------------------------------------
-// charge: fixed-point scale.  F = 35 - e with max|w| in [2^(e-1), 2^e), so
-// |w| 2^F < 2^35 and every contribution (<= |w|/4) rounds to an integer of
-// magnitude below 2^33 (33-bit contributions; precision analysis DESIGN.md §5).
+// charge: fixed-point scale.  F = 33 - e with max|w| in [2^(e-1), 2^e), so
+// |w| 2^F < 2^33 and every contribution (<= |w|/4) rounds to an integer of
+// magnitude below 2^31 (31-bit contributions; precision analysis DESIGN.md §3).
 // ---------------------------------------------------------------------------
 __global__ void k_fx_scale(DevCounters* dc) {
     double wmax = __longlong_as_double((long long)dc->wmax_bits);
-    int F = 35;
+    int F = 33;
     if (wmax > 0.0 && isfinite(wmax)) {
         int e;
         frexp(wmax, &e);  // wmax in [2^(e-1), 2^e)
-        F = 35 - e;
+        F = 33 - e;
     }
     F = max(-60, min(F, 60));
     dc->fx_shift = F;
@@ -292,8 +293,8 @@ struct RingT {
 };
 
 // limbs of the fixed-point value v = round(a*b) taken straight from the bits of
-// t = fma(a, b, 1.5*2^52): the low 17 bits of v are the low 17 bits of t, and
-// v >> 17 (|v| < 2^33) is bits 17..48 of t read as a signed int (the 2^51
+// t = fma(a, b, 1.5*2^52): the low 16 bits of v are the low 16 bits of t, and
+// v >> 16 (|v| < 2^31) is bits 16..47 of t read as a signed int (the 2^51
 // offset of the magic constant vanishes mod 2^32).
 __device__ __forceinline__ double fx_magic(double a, double b) { return __fma_rn(a, b, 6755399441055744.0); }
 __device__ __forceinline__ unsigned fx_lo(double t) { return (unsigned)__double2loint(t) & ((1u << kLimbBits) - 1u); }
