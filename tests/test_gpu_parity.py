@@ -70,7 +70,7 @@ def test_charge_parity_T(G, orc, T, mode):
     ref = orc.charge_global(p, parts)
     assert got.shape == ref.shape
     assert rel_err(got, ref) <= TOL
-    assert rel_err(got, ref) <= 1e-8  # 33-bit fixed-point contributions: far inside TOL
+    assert rel_err(got, ref) <= 1e-8  # 31-bit fixed-point contributions: far inside TOL
 
 
 def test_charge_tiled_equals_direct_bitwise(G, T):
