@@ -300,10 +300,14 @@ def _ngpus():
     return torch.cuda.device_count()
 
 
-@pytest.mark.parametrize("args", [["--size", "T", "--mzetamax", "8"], ["--size", "A", "--nparts", "1000000"]])
+@pytest.mark.parametrize("args", [["--size", "T", "--mzetamax", "8"], ["--size", "A", "--nparts", "1000000"],
+                                  ["--size", "A", "--nparts", "1000000", "--npartdom", "2"],
+                                  ["--size", "A", "--nparts", "1000000", "--nradial", "2", "--precision", "32"]])
 def test_toroidal_decomposition_parity_2gpu(G, args):
-    """Toroidal decomposition over 2 GPUs (NCCL shift, ghost-plane charge
-    merge, halo exchange) against the oracle's single-domain step."""
+    """Decomposition over 2 GPUs against the oracle's single-domain step:
+    toroidal (NCCL shift, ghost-plane charge merge, halo exchange), particle
+    replicas (section charge allreduce, plane-split Poisson) and radial
+    windows with the fp32 state (radial shift)."""
     import os
     import subprocess
     import sys
