@@ -1,7 +1,7 @@
 // Standalone single-GPU harness for the shift kernels (gtcp_shift.cu): times
 // classify / pack / count-holes / backfill on synthetic particles with a given
 // mover fraction, so they can be profiled with ncu without a multi-rank run.
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -I include \
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -I include \
 //   -I <nccl include> -o tools/shift_bench tools/shift_bench.cu paper_1510_05546_b200/csrc/gtcp_shift.cu \
 //   paper_1510_05546_b200/csrc/gtcp_kernels.cu
 #include <cstdio>
@@ -28,9 +28,15 @@ int main(int argc, char** argv) {
     long long n = argc > 1 ? atoll(argv[1]) : 483000000LL;
     double frac = argc > 2 ? atof(argv[2]) : 0.003;
     int reps = argc > 3 ? atoi(argv[3]) : 3;
+    const int mode = argc > 4 ? atoi(argv[4]) : 0;  // 0 toroidal, 1 radial (psi = zeta values here)
     Geo g{};
     g.mzetamax = 64; g.ntor = 2; g.P = 32; g.rank_t = 0;
     g.cz = 64 / GTCP_TWO_PI; g.dzeta = GTCP_TWO_PI / 64;
+    // radial mode: two windows split at r = sqrt(2 * 32 dzeta) (so the zeta
+    // generator's domain edge is the radial boundary in psi)
+    g.nrad = 2; g.rank_r = 0;
+    g.rbound[0] = 0.0; g.rbound[1] = sqrt(2.0 * 32 * g.dzeta); g.rbound[2] = 1e30;
+    for (int b = 0; b < 9; b++) g.rbound2[b] = g.rbound[b] * g.rbound[b];
     const int nattr = 11;
     double* a[11];
     for (int d = 0; d < nattr; d++) cudaMalloc(&a[d], n * sizeof(double));
@@ -55,7 +61,7 @@ int main(int argc, char** argv) {
     for (int r = 0; r < reps; r++) {
         init_zeta<<<148 * 16, 256>>>(a[2], n, frac, 32 * g.dzeta, 7 + r);
         cudaEventRecord(e[0]);
-        launch_shift_classify(g, a[2], n, cls, cL, cR, 0);
+        launch_shift_classify(g, a[2], a[2], mode, n, cls, cL, cR, 0);
         launch_scan_u32(cL, oL, nb, scan_tmp, 0);
         launch_scan_u32(cR, oR, nb, scan_tmp, 0);
         launch_shift_nkeep(n, oL + nb, oR + nb, nkeep, counts, 0);
