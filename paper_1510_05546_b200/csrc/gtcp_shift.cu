@@ -56,21 +56,21 @@ __device__ __forceinline__ void load_cls(const unsigned char* __restrict__ cls, 
     }
 }
 
-// per-byte flag words (0xff / 0x00) -> one bit per byte
-__device__ __forceinline__ unsigned long long flags_to_bits(unsigned f, int i) {
-    const unsigned b = ((f >> 7) & 1u) | ((f >> 14) & 2u) | ((f >> 21) & 4u) | ((f >> 28) & 8u);
-    return (unsigned long long)b << (4 * i);
-}
-// bits of the class bytes equal to v (KIND 0), nonzero (KIND 1), zero (KIND 2)
+// class bytes (0, 1, 2) of a word -> 4 bits (one per byte, bit = predicate):
+// the predicate lands in bit 0 of each byte, then one multiply gathers bits
+// 0, 8, 16, 24 into bits 21..24 (distinct partial products, no carries)
+__device__ __forceinline__ unsigned gather4(unsigned t) { return ((t * 0x00204081u) >> 21) & 0xfu; }
+// bits of the class bytes equal to v in {1, 2} (KIND 0), nonzero (KIND 1), zero (KIND 2)
 template <int KIND>
 __device__ __forceinline__ unsigned long long cls_bits(const unsigned w[kPer / 4], unsigned v = 0) {
     unsigned long long m = 0;
 #pragma unroll
     for (int i = 0; i < kPer / 4; i++) {
-        const unsigned f = KIND == 0 ? __vcmpeq4(w[i], v * 0x01010101u)
-                         : KIND == 1 ? __vcmpne4(w[i], 0u)
-                                     : __vcmpeq4(w[i], 0u);
-        m |= flags_to_bits(f, i);
+        const unsigned x = w[i];
+        const unsigned t = KIND == 0 ? (v == 1u ? (x & ~(x >> 1)) : ((x >> 1) & ~x)) & 0x01010101u
+                         : KIND == 1 ? (x | (x >> 1)) & 0x01010101u
+                                     : ~(x | (x >> 1)) & 0x01010101u;
+        m |= (unsigned long long)gather4(t) << (4 * i);
     }
     return m;
 }
@@ -157,25 +157,32 @@ __global__ void __launch_bounds__(kLT) k_shift_classify(Geo g, const double* __r
     constexpr int kWarps = kLT / 32, kSlice = kChunk / kWarps;
     const R* key = reinterpret_cast<const R*>(mode ? psi : zeta);
     unsigned a = 0, b = 0;
-#pragma unroll 8
-    for (int it = 0; it < kSlice / 32; it++) {
-        const long long p = base + (long long)w * kSlice + it * 32 + lane;
-        unsigned char c = 0;
-        if (p < n) {
-            const double z = (double)__ldcs(key + p);
-            if (mode == 0) {
-                int d = shift_plane(g, z) / g.P;
-                int rel = d - g.rank_t;
-                if (rel < 0) rel += g.ntor;
-                if (rel != 0) c = (rel <= g.ntor / 2) ? 2 : 1;
-            } else {
-                int rel = radial_domain(g, z) - g.rank_r;
-                if (rel != 0) c = (rel > 0) ? 2 : 1;
+    // batches of kB independent loads in flight per warp, then the decisions
+    constexpr int kB = 8;
+    for (int it0 = 0; it0 < kSlice / 32; it0 += kB) {
+        const long long p0 = base + (long long)w * kSlice + it0 * 32 + lane;
+        double z[kB];
+#pragma unroll
+        for (int j = 0; j < kB; j++) z[j] = p0 + 32 * j < n ? (double)__ldcs(key + p0 + 32 * j) : 0.0;
+#pragma unroll
+        for (int j = 0; j < kB; j++) {
+            const long long p = p0 + 32 * j;
+            unsigned char c = 0;
+            if (p < n) {
+                if (mode == 0) {
+                    int d = shift_plane(g, z[j]) / g.P;
+                    int rel = d - g.rank_t;
+                    if (rel < 0) rel += g.ntor;
+                    if (rel != 0) c = (rel <= g.ntor / 2) ? 2 : 1;
+                } else {
+                    int rel = radial_domain(g, z[j]) - g.rank_r;
+                    if (rel != 0) c = (rel > 0) ? 2 : 1;
+                }
+                cls[p] = c;
             }
-            cls[p] = c;
+            a += __popc(__ballot_sync(0xffffffffu, c == 1));
+            b += __popc(__ballot_sync(0xffffffffu, c == 2));
         }
-        a += __popc(__ballot_sync(0xffffffffu, c == 1));
-        b += __popc(__ballot_sync(0xffffffffu, c == 2));
     }
     unsigned ta, tb;
     block_excl_scan(lane == 0 ? a : 0u, sw, &ta);
