@@ -84,6 +84,8 @@ def lib():
                                      C.c_int32, C.c_int32, d]),
             "orc_shift_dest": (None, [P, C.c_int64, d, C.c_int32, i32]),
             "orc_bin_key": (None, [P, C.c_int64, d, d, d, d, C.c_int32, C.c_int32, C.c_int32, i64]),
+            "orc_radial_windows": (None, [P, C.c_int32, i32]),
+            "orc_radial_dest": (None, [P, C.c_int64, d, C.c_int32, i32, i32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -237,6 +239,23 @@ def shift_dest(p: Params, zeta: np.ndarray, P: int) -> np.ndarray:
     z = _f64(zeta)
     out = np.zeros(len(z), np.int32)
     lib().orc_shift_dest(C.byref(p), len(z), _d(z), P, out.ctypes.data_as(C.POINTER(C.c_int32)))
+    return out
+
+
+def radial_windows(p: Params, K: int) -> np.ndarray:
+    """G-6 equal-area radial windows snapped to rings: ring indices bound[0..K]."""
+    out = np.zeros(K + 1, np.int32)
+    lib().orc_radial_windows(C.byref(p), K, out.ctypes.data_as(C.POINTER(C.c_int32)))
+    return out
+
+
+def radial_dest(p: Params, psi: np.ndarray, K: int) -> np.ndarray:
+    """H-2 radial owner window of each particle (G-6 windows)."""
+    b = radial_windows(p, K)
+    z = _f64(psi)
+    out = np.zeros(len(z), np.int32)
+    lib().orc_radial_dest(C.byref(p), len(z), _d(z), K, b.ctypes.data_as(C.POINTER(C.c_int32)),
+                          out.ctypes.data_as(C.POINTER(C.c_int32)))
     return out
 
 

@@ -310,7 +310,10 @@ static double plane_interp(const orc_params* p, const orc_geom* g, const double*
 
 /* F-1: four-point gyro-average operator on one plane with radius
  * rho_G = sqrt(2)/omega0 (so that G^2 ~ Gamma_0 to O(b)).  Parity:
- * pinned by "constant in -> constant out" and the rho -> 0 limit tests. */
+ * pinned by "constant in -> constant out", G(r) = r, the rho -> 0 limit,
+ * G(r^2) = r^2 + rho_G^2/2 (radius) and second-order convergence of
+ * G cos(m theta) to cos(m theta)[1/2 + 1/2 cos(m rho_G/r)] (angular offset
+ * rho_G/r) -- tests/test_oracle_closed_forms.py. */
 static void gyro_op(const orc_params* p, const orc_geom* g, const double* in, double* out,
                     int32_t k) {
     double zeta_k = k * (TWO_PI / p->mzetamax);
@@ -359,8 +362,10 @@ static double plane_value(const orc_params* p, const orc_geom* g, const double* 
 /* F-4 smooth (reading; "a filter"): one (1/4,1/2,1/4) pass along theta
  * (periodic), then along r at the same physical angle (boundary rings
  * fixed), then along the field line (same label, neighbouring planes, seam
- * rotation).  Pinned: constants are preserved; the theta pass preserves ring
- * sums (tests). */
+ * rotation).  Pinned: constants preserved, linearity, the exact response
+ * 1/2 + 1/2 cos(2 pi m/mt) of a ring Fourier mode with the seam-rotated
+ * parallel pass on planes 0 and K-1, and r^2 -> r^2 + dr^2/2 for the radial
+ * pass (tests/test_oracle_closed_forms.py). */
 void orc_smooth(const orc_params* p, double* f) {
     orc_geom g;
     geom_build(p, &g);
@@ -546,7 +551,10 @@ void orc_gyro_op(const orc_params* p, int32_t k, const double* in, double* out) 
  *   g_th  = (phi_{j+1} - phi_{j-1}) / (2 dtheta_i), periodic;
  *   g_par = (phi(k+1) - phi(k-1)) / (2 dzeta) at the same label (seam rotation).
  * Pinned: constant phi -> 0; sin(m theta) -> second-order convergent g_theta;
- * linear-in-r phi -> exact g_r; field-line-constant phi -> g_par = 0. */
+ * linear-in-r phi -> exact g_r; r cos(theta) -> g_r = cos(theta) at the
+ * physical angle (second order); cos(n theta - l zeta) -> second-order
+ * g_par on every plane, through the seam rotation
+ * (tests/test_oracle_grid.py, tests/test_oracle_closed_forms.py). */
 void orc_field(const orc_params* p, const double* phi, double* gradphi) {
     orc_geom g;
     geom_build(p, &g);
@@ -663,7 +671,9 @@ void orc_rhs(const orc_params* p, const double* X, double mu, const double* gbar
 }
 
 /* U-8: wrap theta, zeta into [0, 2 pi); reflect r at a0, a1 (reading A-17).
- * Returns 1 if a reflection happened. */
+ * Returns 1 if a reflection happened.  Pinned: one outward and one inward
+ * crossing against the closed form r' = 2 a1 - r / 2 a0 - r
+ * (tests/test_oracle_closed_forms.py). */
 static int orc_post(const orc_params* p, double* X) {
     double t = X[1] - TWO_PI * floor(X[1] / TWO_PI);
     if (t >= TWO_PI) t = 0.0;
@@ -722,6 +732,44 @@ void orc_shift_dest(const orc_params* p, int64_t n, const double* zeta, int32_t 
         double wz1;
         orc_plane(p, zeta[ip], &kg, &wz1);
         dest[ip] = kg / P;
+    }
+}
+
+/* G-6 ("the radial domain decomposition ... each subdomain has
+ * roughly the same area"): K radial windows split the
+ * annulus a0 < r < a1 into equal areas, r_k = sqrt(a0^2 + (k/K)(a1^2 - a0^2)),
+ * each boundary snapped to the nearest ring (floor((r_k - a0)/dr + 1/2)).
+ * bound[0..K] are ring indices, bound[0] = 0, bound[K] = mpsi.
+ * Pinned: class D at K = 2 splits at ring 519 with owned sum(mtheta)
+ * 1,201,004 / 1,205,110 (SURVEY G-6 [computed]); exact-decimal recomputation
+ * of the snapped boundaries (tests/test_oracle_radial.py). */
+void orc_radial_windows(const orc_params* p, int32_t K, int32_t* bound) {
+    double dr = orc_dr(p);
+    bound[0] = 0;
+    for (int32_t k = 1; k < K; k++) {
+        double rk = sqrt(p->a0 * p->a0 + ((double)k / K) * (p->a1 * p->a1 - p->a0 * p->a0));
+        int32_t b = (int32_t)floor((rk - p->a0) / dr + 0.5);
+        if (b < 0) b = 0;
+        if (b > p->mpsi) b = p->mpsi;
+        bound[k] = b;
+    }
+    bound[K] = p->mpsi;
+}
+
+/* H-2 (P:244-249 radial domains; SPEC S:553 toroidal first, then radial):
+ * radial owner of each particle = the window k whose boundary radii bracket
+ * its gyrocentre radius r = sqrt(2 psi): r(bound[k]) <= r < r(bound[k+1]),
+ * r(b) = a0 + b dr; the last window also owns r = a1.  Pinned against an
+ * exact-decimal brute-force owner test (tests/test_oracle_radial.py). */
+void orc_radial_dest(const orc_params* p, int64_t n, const double* psi, int32_t K, const int32_t* bound,
+                     int32_t* dest) {
+    double dr = orc_dr(p);
+    for (int64_t ip = 0; ip < n; ip++) {
+        double r = sqrt(2.0 * psi[ip]);
+        int32_t d = 0;
+        for (int32_t k = 1; k < K; k++)
+            if (r >= p->a0 + bound[k] * dr) d = k;
+        dest[ip] = d;
     }
 }
 
