@@ -101,10 +101,26 @@ def dist_env():
     return rank, world, local
 
 
-def cpu_baseline(size: str, n_sample: int, steps: int = 1):
-    """Oracle (single-threaded C, fp64) charge + push + shift on a bounded
-    sample of the workload's markers, on the workload's full grid, with a
-    fixed prescribed field.  Returns particle-steps/s and the time."""
+def host_info() -> dict:
+    """nproc and the CPU model of the box the oracle runs on."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "lscpu_model": model}
+
+
+def cpu_baseline(size: str, n_sample: int, steps: int = 1, parallel: bool = True):
+    """Oracle (C, fp64) charge + push + shift on a bounded sample of the
+    workload's markers, on the workload's full grid, with a fixed prescribed
+    field.  parallel: the paper's CPU method on all host cores (OpenMP threads
+    over particle ranges, per-thread grid replicas summed in a fixed order,
+    P:330); else one thread.  Returns (particle-steps/s, seconds, threads)."""
     import numpy as np
 
     import oracle
@@ -118,15 +134,19 @@ def cpu_baseline(size: str, n_sample: int, steps: int = 1):
     gp = 1e-3 * rng.standard_normal((K + 1, g.mgrid, 3))
     Xa = {k: parts[k].copy() for k in oracle.ATTRS}
     Xb = {k: v.copy() for k, v in Xa.items()}
+    dep = oracle.deposit_replicas if parallel else oracle.deposit
+    push = oracle.push_omp if parallel else oracle.push
+    dest = oracle.shift_dest_omp if parallel else oracle.shift_dest
     t0 = time.perf_counter()
     for _ in range(steps):
         for stage in (1, 2):
             cur = dict(Xa if stage == 1 else Xb, mu=parts["mu"])
-            oracle.charge_global(p, cur)
-            oracle.push(p, stage, Xa, Xb, parts["mu"], gp)
-            oracle.shift_dest(p, (Xb if stage == 1 else Xa)["zeta"], K)
+            grid, _ = dep(p, cur)
+            oracle.charge_reduce_global(p, grid)
+            push(p, stage, Xa, Xb, parts["mu"], gp)
+            dest(p, (Xb if stage == 1 else Xa)["zeta"], K)
     dt = time.perf_counter() - t0
-    return n_sample * steps / dt, dt
+    return n_sample * steps / dt, dt, (oracle.omp_threads() if parallel else 1)
 
 
 def workload_config(size: str, n_gpus: int, args) -> dict:
@@ -135,13 +155,14 @@ def workload_config(size: str, n_gpus: int, args) -> dict:
     import synth
     over = {"micell": args.micell} if args.micell else {}
     cfg = synth.config(size, **over)
-    import oracle
-    g = oracle.geometry(oracle.make_params(cfg))
+    # grid size from the product's host geometry (G-1..G-2); no oracle here
+    import paper_1510_05546_b200 as G
+    mgrid = G.gtcp_geometry(G.gtcp_default_params(size, **over))["mgrid"]
     ntor = max(1, n_gpus // (args.nradial * args.npartdom))
     return {"workload": f"GTC-P class {size}: mpsi={cfg['mpsi']} mthetamax={cfg['mthetamax']} "
                         f"mzetamax={cfg['mzetamax']} micell={cfg['micell']}",
-            "particles": int(cfg["micell"] * (g.mgrid - cfg["mpsi"]) * cfg["mzetamax"]),
-            "grid_nodes_per_plane": int(g.mgrid), "planes": cfg["mzetamax"],
+            "particles": int(cfg["micell"] * (mgrid - cfg["mpsi"]) * cfg["mzetamax"]),
+            "grid_nodes_per_plane": int(mgrid), "planes": cfg["mzetamax"],
             "decomposition": f"{ntor} toroidal x {args.nradial} radial x {args.npartdom} particle"}
 
 
@@ -155,7 +176,7 @@ def run_reference(args):
     oracle.build()
     vals = []
     for i in range(args.warmup + args.steps):
-        v, dt = cpu_baseline(size, n_sample, 1)
+        v, dt, nthr = cpu_baseline(size, n_sample, 1)
         if i >= args.warmup:
             vals.append((v, dt))
     total_t = sum(dt for _, dt in vals)
@@ -166,9 +187,11 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": workload_config(size, args.gpus, args),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthr, "kind": "oracle",
                          "sample": f"{n_sample} markers of class {size} on its full grid, charge+push+shift, "
-                                   f"fixed prescribed field, {len(vals)} steps"},
+                                   f"fixed prescribed field, {len(vals)} steps; OpenMP over {nthr} threads with "
+                                   f"per-thread grid replicas summed in a fixed order (P:330)",
+                         "host": host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -286,30 +309,48 @@ def run_gpu(args):
     if not args.no_e2e:
         k_e2e = max(1, min(args.steps, args.e2e_steps))
         parts = ctx.get_particles(("psi", "theta", "zeta", "rho", "w", "mu"))
-        host = [torch.from_numpy(parts[k]).pin_memory().numpy() for k in ("psi", "theta", "zeta", "rho", "w", "mu")]
+        n_e2e = len(parts["psi"])
+        cap = ctx.get_info().capacity  # the owned count may change under a decomposed run
+        host = []
+        for k in ("psi", "theta", "zeta", "rho", "w", "mu"):
+            a = torch.empty(cap, dtype=torch.float64).pin_memory().numpy()
+            a[:n_e2e] = parts[k]
+            host.append(a)
         del parts
         ctx.set_timing(False)
         barrier()
         t0 = time.perf_counter()
+        h2d = d2h = 0
         for _ in range(k_e2e):
-            ctx.step_host(host, 1)
+            h2d += 6 * 8 * n_e2e
+            n_e2e = ctx.step_host(host, 1, n_e2e)
+            d2h += 6 * 8 * n_e2e
         barrier()
         dt = time.perf_counter() - t0
         if dist:
             t = torch.tensor([dt], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
-        e2e = {"value": n_total * k_e2e / dt, "unit": UNIT, "h2d_bytes_per_step": int(6 * 8 * n_total),
-               "d2h_bytes_per_step": int(5 * 8 * n_total), "steps": k_e2e,
-               "how": "gtcp_step_host: pinned host SoA -> device, one step, device -> host, per step"}
+        if dist:
+            t = torch.tensor([h2d, d2h], dtype=torch.int64, device="cuda")
+            dist.all_reduce(t)
+            h2d, d2h = int(t[0].item()), int(t[1].item())
+        e2e = {"value": n_total * k_e2e / dt, "unit": UNIT, "h2d_bytes_per_step": h2d // k_e2e,
+               "d2h_bytes_per_step": d2h // k_e2e, "steps": k_e2e,
+               "how": "gtcp_step_host: pinned host SoA (live state + mu) -> device, one step, "
+                      "device -> host (live state + mu), per step, all ranks"}
     out = None
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu:
-            v, dt = cpu_baseline(size, args.ref_sample, 1)
-            cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+            v, dt, nthr = cpu_baseline(size, args.ref_sample, 1, parallel=True)
+            v1, dt1, _ = cpu_baseline(size, args.ref_sample // 4, 1, parallel=False)
+            cpu = {"value": v, "unit": UNIT, "cores": nthr, "kind": "oracle",
                    "sample": f"{args.ref_sample} markers of class {size} on its full grid, one step of "
-                             f"charge+push+shift with a fixed field ({dt:.1f} s single-threaded)"}
+                             f"charge+push+shift with a fixed field ({dt:.1f} s on {nthr} OpenMP threads, "
+                             f"per-thread grid replicas summed in a fixed order, P:330)",
+                   "single_thread": {"value": v1, "sample": f"{args.ref_sample // 4} markers, {dt1:.1f} s"},
+                   "host": host_info()}
         r = roof.get(dom, {})
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -149,6 +149,10 @@ typedef struct {
     double ms[GTCP_NPHASE];
     int64_t calls[GTCP_NPHASE];
     int64_t launches;       /* kernels launched by the library (all phases)     */
+    int64_t comm_bytes[GTCP_NPHASE]; /* bytes this rank moved between GPUs per phase,
+                             * counted by the library (NCCL bus-byte convention:
+                             * send/recv payload, allreduce 2(n-1)/n x size,
+                             * broadcast size); 0 on one GPU                    */
 } gtcp_timings_t;
 
 /* Fill *out with the preset of size 'T','A','B','C','D' (BASELINE.json
@@ -210,17 +214,27 @@ gtcp_status gtcp_field(gtcp_ctx ctx);
  * ESTATE if stage is not the one expected. */
 gtcp_status gtcp_push(gtcp_ctx ctx, int stage);
 /* Migrate particles to their owner domain (H-1 toroidal, then H-2 radial;
- * multi-hop with guard), then bin by cell when the schedule says so (after
- * stage 2 every bin_every steps). */
+ * multi-hop with guard: GTCP_EINVARIANT if movers remain after ntoroidal + 1
+ * passes), then bin by cell when the schedule says so (after stage 2 every
+ * bin_every steps).  ECAPACITY on a send-buffer or particle-capacity overflow. */
 gtcp_status gtcp_shift(gtcp_ctx ctx);
 /* Force a bin (cell sort, H-4) now. */
 gtcp_status gtcp_bin(gtcp_ctx ctx);
-/* nsteps x [for stage in (1,2): charge, poisson_smooth, field, push(stage), shift]. */
+/* nsteps x [for stage in (1,2): charge, poisson_smooth, field, push(stage), shift].
+ * Synchronises the stream once at the end and returns GTCP_ENONFINITE if a
+ * push produced a non-finite state (checked without waiting after every
+ * step as well, so a long call stops within about a step of the event). */
 gtcp_status gtcp_step(gtcp_ctx ctx, int nsteps);
 /* End-to-end offload call: upload n particles from host buffers attr[0..6)
- * (live state + mu), run nsteps steps, download the live state back into the
- * same buffers.  Synchronises. */
-gtcp_status gtcp_step_host(gtcp_ctx ctx, int64_t n, double* const* attr, int nsteps);
+ * (live state + mu), run nsteps steps, download the owned particles' live
+ * state AND mu (a bin or a shift inside the steps reorders them together)
+ * back into the same buffers, whose capacity is cap elements each.
+ * *n_out = the owned count after the steps (differs from n when a decomposed
+ * run migrated particles).  ECAPACITY, with nothing downloaded, if that count
+ * exceeds cap.  The tiles of the previous bin are kept: they are exact for a
+ * state returned by the previous call (same order); any other order stays
+ * exact through the deposit's out-of-window path, only slower.  Synchronises. */
+gtcp_status gtcp_step_host(gtcp_ctx ctx, int64_t n, int64_t cap, double* const* attr, int nsteps, int64_t* n_out);
 
 gtcp_status gtcp_get_grid(gtcp_ctx ctx, int which, int64_t cap, double* host);
 /* Prescribe a grid (tests): CHARGE (then poisson_smooth uses it), PHI (then
@@ -232,6 +246,23 @@ gtcp_status gtcp_timings(gtcp_ctx ctx, gtcp_timings_t* out);
 gtcp_status gtcp_timings_reset(gtcp_ctx ctx);
 /* Enable (1) / disable (0) per-phase CUDA-event timing (default off). */
 gtcp_status gtcp_set_timing(gtcp_ctx ctx, int enable);
+
+/* Test-only transport (SURVEY §4 "loopback"): nranks contexts of ONE process
+ * on ONE device, one host thread per context, share a hub instead of NCCL.
+ * Every exchange of the decomposed step (ghost-plane charge merge, section
+ * and ring allreduces, potential halos, Poisson plane broadcasts, shift
+ * counts and payload) then runs as one cudaMemcpyAsync per message between
+ * the contexts' device buffers (allreduce: one small kernel summing the
+ * members' staged buffers in member order), so the decomposition can be
+ * parity-checked on a single GPU.  gtcp_loopback_create returns the hub
+ * (EINVAL for nranks outside 1..16); gtcp_init_loopback is gtcp_init with the
+ * hub in place of the NCCL id (same rank layout and invariants; the stream
+ * should be a distinct non-blocking stream per context).  The hub must
+ * outlive every context created on it; gtcp_loopback_destroy frees it. */
+gtcp_status gtcp_loopback_create(int nranks, void** hub);
+void gtcp_loopback_destroy(void* hub);
+gtcp_status gtcp_init_loopback(const gtcp_params* p, int rank, int nranks, void* hub, void* cuda_stream,
+                               gtcp_ctx* out);
 
 /* Test hooks: select the charge kernel (0 = smem-tiled, 1 = direct global
  * fixed-point atomics) -- both are product CUDA paths. */

@@ -19,16 +19,18 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "gtcp_oracle.c")
+_SRC_OMP = os.path.join(_HERE, "gtcp_oracle_omp.c")
 _LIB_PATH = os.path.join(_HERE, "_build", "liboracle.so")
 
 
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc (fp64, -ffp-contract=off: no fused a*b+c)."""
     os.makedirs(os.path.dirname(_LIB_PATH), exist_ok=True)
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB_PATH) or \
+            os.path.getmtime(_LIB_PATH) < max(os.path.getmtime(_SRC), os.path.getmtime(_SRC_OMP)):
         tmp = _LIB_PATH + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math",
-                               "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+                               "-fPIC", "-shared", "-o", tmp, _SRC, _SRC_OMP, "-lm"])
         os.replace(tmp, _LIB_PATH)
     return _LIB_PATH
 
@@ -84,6 +86,11 @@ def lib():
                                      C.c_int32, C.c_int32, d]),
             "orc_shift_dest": (None, [P, C.c_int64, d, C.c_int32, i32]),
             "orc_bin_key": (None, [P, C.c_int64, d, d, d, d, C.c_int32, C.c_int32, C.c_int32, i64]),
+            "orc_omp_threads": (C.c_int, []),
+            "orc_deposit_replicas": (C.c_int64, [P, C.c_int64, d, d, d, d, d, C.c_int32, C.c_int32, d, C.c_int64]),
+            "orc_push_omp": (C.c_int64, [P, C.c_int32, C.c_int64, C.POINTER(d), C.POINTER(d), d,
+                                         C.c_int32, C.c_int32, d]),
+            "orc_shift_dest_omp": (None, [P, C.c_int64, d, C.c_int32, i32]),
             "orc_radial_windows": (None, [P, C.c_int32, i32]),
             "orc_radial_dest": (None, [P, C.c_int64, d, C.c_int32, i32, i32]),
         }
@@ -239,6 +246,40 @@ def shift_dest(p: Params, zeta: np.ndarray, P: int) -> np.ndarray:
     z = _f64(zeta)
     out = np.zeros(len(z), np.int32)
     lib().orc_shift_dest(C.byref(p), len(z), _d(z), P, out.ctypes.data_as(C.POINTER(C.c_int32)))
+    return out
+
+
+def omp_threads() -> int:
+    return int(lib().orc_omp_threads())
+
+
+def deposit_replicas(p: Params, parts: dict, k0: int = 0, P: int | None = None):
+    """orc_deposit over all OpenMP threads with per-thread grid replicas summed
+    in thread order; same result as deposit() up to summation order."""
+    g = geometry(p)
+    P = p.mzetamax if P is None else P
+    grid = np.zeros((P + 1) * g.mgrid)
+    a = [_f64(parts[k]) for k in ("psi", "theta", "zeta", "mu", "w")]
+    nclamp = lib().orc_deposit_replicas(C.byref(p), len(a[0]), *[_d(x) for x in a], k0, P, _d(grid), grid.size)
+    return grid.reshape(P + 1, g.mgrid), nclamp
+
+
+def push_omp(p: Params, stage: int, Xa: dict, Xb: dict, mu, gradphi, k0: int = 0, P: int | None = None) -> int:
+    """push() split over all OpenMP threads by particle range."""
+    P = p.mzetamax if P is None else P
+    for dct in (Xa, Xb):
+        for k in ATTRS:
+            dct[k] = _f64(dct[k])
+    pa = (C.POINTER(C.c_double) * 5)(*[_d(Xa[k]) for k in ATTRS])
+    pb = (C.POINTER(C.c_double) * 5)(*[_d(Xb[k]) for k in ATTRS])
+    mu = _f64(mu)
+    return lib().orc_push_omp(C.byref(p), stage, len(mu), pa, pb, _d(mu), k0, P, _d(_f64(gradphi).ravel()))
+
+
+def shift_dest_omp(p: Params, zeta: np.ndarray, P: int) -> np.ndarray:
+    z = _f64(zeta)
+    out = np.zeros(len(z), np.int32)
+    lib().orc_shift_dest_omp(C.byref(p), len(z), _d(z), P, out.ctypes.data_as(C.POINTER(C.c_int32)))
     return out
 
 

@@ -60,7 +60,8 @@ class Stats(C.Structure):
 
 
 class Timings(C.Structure):
-    _fields_ = [("ms", C.c_double * 7), ("calls", C.c_int64 * 7), ("launches", C.c_int64)]
+    _fields_ = [("ms", C.c_double * 7), ("calls", C.c_int64 * 7), ("launches", C.c_int64),
+                ("comm_bytes", C.c_int64 * 7)]
 
 
 # every symbol declared in include/gtcp.h
@@ -68,7 +69,8 @@ SYMBOLS = ("gtcp_default_params", "gtcp_geometry", "gtcp_nccl_unique_id", "gtcp_
            "gtcp_strerror", "gtcp_info", "gtcp_load", "gtcp_set_particles", "gtcp_get_particles", "gtcp_charge",
            "gtcp_poisson_smooth", "gtcp_field", "gtcp_push", "gtcp_shift", "gtcp_bin", "gtcp_step",
            "gtcp_step_host", "gtcp_get_grid", "gtcp_set_grid", "gtcp_stats", "gtcp_timings", "gtcp_timings_reset",
-           "gtcp_set_timing", "gtcp_set_charge_mode", "gtcp_sample_particles")
+           "gtcp_set_timing", "gtcp_set_charge_mode", "gtcp_sample_particles", "gtcp_loopback_create",
+           "gtcp_loopback_destroy", "gtcp_init_loopback")
 
 _lib = None
 
@@ -102,7 +104,10 @@ def lib():
             "gtcp_shift": (st, [vp]),
             "gtcp_bin": (st, [vp]),
             "gtcp_step": (st, [vp, C.c_int]),
-            "gtcp_step_host": (st, [vp, C.c_int64, dpp, C.c_int]),
+            "gtcp_step_host": (st, [vp, C.c_int64, C.c_int64, dpp, C.c_int, C.POINTER(C.c_int64)]),
+            "gtcp_loopback_create": (st, [C.c_int, C.POINTER(vp)]),
+            "gtcp_loopback_destroy": (None, [vp]),
+            "gtcp_init_loopback": (st, [C.POINTER(Params), C.c_int, C.c_int, vp, vp, C.POINTER(vp)]),
             "gtcp_get_grid": (st, [vp, C.c_int, C.c_int64, C.POINTER(C.c_double)]),
             "gtcp_set_grid": (st, [vp, C.c_int, C.c_int64, C.POINTER(C.c_double)]),
             "gtcp_stats": (st, [vp, C.POINTER(Stats)]),
@@ -161,11 +166,15 @@ class Context:
     """One rank's GTC-P hot-path state on the current CUDA device (gtcp_init)."""
 
     def __init__(self, params: Params, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None,
-                 stream: int | None = None):
+                 stream: int | None = None, loopback: "LoopbackHub | None" = None):
         self.params = params
         self._h = C.c_void_p()
-        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
-        s = lib().gtcp_init(C.byref(params), rank, nranks, idbuf, C.c_void_p(stream or 0), C.byref(self._h))
+        if loopback is not None:
+            s = lib().gtcp_init_loopback(C.byref(params), rank, nranks, loopback.handle, C.c_void_p(stream or 0),
+                                         C.byref(self._h))
+        else:
+            idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+            s = lib().gtcp_init(C.byref(params), rank, nranks, idbuf, C.c_void_p(stream or 0), C.byref(self._h))
         if s:
             msg = lib().gtcp_strerror(self._h).decode() if self._h.value else ""
             if self._h.value:
@@ -258,11 +267,16 @@ class Context:
     def step(self, nsteps: int = 1):
         self._chk(lib().gtcp_step(self._h, nsteps), "step")
 
-    def step_host(self, arrays: list, nsteps: int = 1):
-        """arrays: 6 pinned/contiguous fp64 host arrays (psi, theta, zeta, rho, w, mu); updated in place."""
-        n = len(arrays[0])
+    def step_host(self, arrays: list, nsteps: int = 1, n: int | None = None) -> int:
+        """arrays: 6 pinned/contiguous fp64 host arrays (psi, theta, zeta, rho, w, mu) of equal capacity;
+        the first n (default: all) are uploaded, the owned particles after the steps (live state and mu)
+        are written back in place.  Returns the owned count."""
+        cap = len(arrays[0])
+        n = cap if n is None else n
         ptrs = (C.POINTER(C.c_double) * 6)(*[_dp(a) for a in arrays])
-        self._chk(lib().gtcp_step_host(self._h, n, ptrs, nsteps), "step_host")
+        nout = C.c_int64()
+        self._chk(lib().gtcp_step_host(self._h, n, cap, ptrs, nsteps, C.byref(nout)), "step_host")
+        return int(nout.value)
 
     # -- grids
     def _grid_len(self, which: int) -> int:
@@ -298,6 +312,7 @@ class Context:
         self._chk(lib().gtcp_timings(self._h, C.byref(t)), "timings")
         d = {f"{p}_ms": t.ms[i] for i, p in enumerate(PHASES)}
         d.update({f"{p}_calls": t.calls[i] for i, p in enumerate(PHASES)})
+        d.update({f"{p}_comm_bytes": t.comm_bytes[i] for i, p in enumerate(PHASES)})
         d["launches"] = t.launches
         return d
 
@@ -306,6 +321,24 @@ class Context:
 
     def set_charge_mode(self, mode: int):
         self._chk(lib().gtcp_set_charge_mode(self._h, mode), "set_charge_mode")
+
+
+class LoopbackHub:
+    """Test-only in-process transport (gtcp_loopback_create): nranks contexts
+    of one process on one device share it instead of an NCCL id; drive each
+    context from its own host thread on its own stream."""
+
+    def __init__(self, nranks: int):
+        self.handle = C.c_void_p()
+        s = lib().gtcp_loopback_create(nranks, C.byref(self.handle))
+        if s:
+            raise GtcpError(s, "loopback_create")
+        self.nranks = nranks
+
+    def close(self):
+        if self.handle and self.handle.value:
+            lib().gtcp_loopback_destroy(self.handle)
+            self.handle = C.c_void_p()
 
 
 # module-level names matching the C ABI

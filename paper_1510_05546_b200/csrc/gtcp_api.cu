@@ -20,10 +20,13 @@ struct gtcp_ctx_s {
     gtcp_params prm;
     int rank, nranks, rank_t, rank_p, rank_r;
     std::vector<int> rad_ring;    // radial window boundaries (ring indices), nradial+1
-    ncclComm_t sect = nullptr, rad = nullptr;  // same toroidal domain; same (toroidal, replica)
+    Comm sect, rad;  // same toroidal domain; same (toroidal, replica)
     cudaStream_t st;
     int device;
-    ncclComm_t world = nullptr, tor = nullptr, part = nullptr;
+    Comm world, tor;  // all ranks; toroidal ring (same radial window and replica)
+    LoopHub* hub = nullptr;  // loopback transport (test-only), not owned
+    long long comm_bytes[GTCP_NPHASE] = {};  // bytes moved by this rank per phase (NCCL bus-byte convention)
+    int cur_phase = GTCP_T_CHARGE_RED;       // phase the comm calls are charged to
     std::string err;
     gtcp_status sticky = GTCP_OK;
     // geometry (host + device)
@@ -68,6 +71,7 @@ struct gtcp_ctx_s {
     long long* fx_recv = nullptr;  // mgrid
     DevCounters* dc = nullptr;
     DevCounters* h_dc = nullptr;  // pinned host mirror
+    int* h_nonfinite = nullptr;   // pinned mirror of dc->nonfinite, refreshed after every push
     double* d_scalar = nullptr;   // small device scratch (sums)
     double* d_partial = nullptr;  // 1024 partial sums
     double* h_scalar = nullptr;   // pinned
@@ -124,7 +128,7 @@ static gtcp_status set_err(gtcp_ctx c, gtcp_status s, const std::string& msg) {
     do {                                                                                           \
         ncclResult_t _r = (call);                                                                  \
         if (_r != ncclSuccess)                                                                     \
-            return set_err(c, GTCP_ENCCL, std::string(#call) + ": " + ncclGetErrorString(_r));     \
+            return set_err(c, GTCP_ENCCL, std::string(#call) + ": " + comm_error_string(_r));      \
     } while (0)
 #define CHECK_CTX(c)                                                                               \
     do {                                                                                           \
@@ -169,13 +173,17 @@ struct PhaseTimer {
     gtcp_ctx c;
     int phase;
     cudaEvent_t a = nullptr;
+    int prev_phase;
     PhaseTimer(gtcp_ctx c_, int ph) : c(c_), phase(ph) {
+        prev_phase = c->cur_phase;
+        c->cur_phase = ph;
         if (c->timing) {
             a = get_event(c);
             cudaEventRecord(a, c->st);
         }
     }
     ~PhaseTimer() {
+        c->cur_phase = prev_phase;
         if (c->timing) {
             cudaEvent_t b = get_event(c);
             cudaEventRecord(b, c->st);
@@ -271,8 +279,8 @@ static cudaError_t dalloc(T** p, size_t count) {
     return cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T));
 }
 
-extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, const void* nccl_id,
-                                 void* cuda_stream, gtcp_ctx* out) {
+static gtcp_status init_ctx(const gtcp_params* p, int rank, int nranks, const void* nccl_id, LoopHub* hub,
+                            void* cuda_stream, gtcp_ctx* out) {
     if (!p || !out || nranks < 1 || rank < 0 || rank >= nranks) return GTCP_EINVAL;
     if (p->precision != 64 && p->precision != 32) return GTCP_EINVAL;
     if (p->mpsi < 2 || p->mthetamax < 4 || p->mzetamax < 2 || p->micell < 0) return GTCP_EINVAL;
@@ -281,7 +289,8 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     if (p->bin_mu < 1 || p->bin_mu > 16) return GTCP_EINVAL;
     if (p->mzetamax % p->ntoroidal != 0 || p->ntoroidal * nrad * p->npartdom != nranks) return GTCP_EINVARIANT;
     if (p->mzetamax / p->ntoroidal < 2) return GTCP_EINVARIANT;
-    if (nranks > 1 && !nccl_id) return GTCP_EINVAL;
+    if (nranks > 1 && !nccl_id && !hub) return GTCP_EINVAL;
+    if (hub && loop_hub_size(hub) != nranks) return GTCP_EINVAL;
     gtcp_ctx c = new gtcp_ctx_s();
     c->prm = *p;
     c->prm.nradial = nrad;
@@ -443,6 +452,8 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     CU(dalloc(&c->dc, 1));
     CU(cudaMemset(c->dc, 0, sizeof(DevCounters)));
     CU(cudaMallocHost((void**)&c->h_dc, sizeof(DevCounters)));
+    CU(cudaMallocHost((void**)&c->h_nonfinite, sizeof(int)));
+    c->h_nonfinite[0] = 0;
     CU(dalloc(&c->d_scalar, 16));
     CU(dalloc(&c->d_partial, 1024));
     CU(cudaMallocHost((void**)&c->h_scalar, 16 * sizeof(double)));
@@ -484,14 +495,19 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     c->launches0 = gtcp::g_launches;
     // NCCL communicators
     if (nranks > 1) {
-        ncclUniqueId uid;
-        memcpy(&uid, nccl_id, sizeof(uid));
-        NC(ncclCommInitRank(&c->world, nranks, uid, rank));
+        if (hub) {
+            c->hub = hub;
+            c->world = loop_world(hub, rank);
+        } else {
+            ncclUniqueId uid;
+            memcpy(&uid, nccl_id, sizeof(uid));
+            NC(comm_init_nccl(&c->world, nranks, uid, rank));
+        }
         // toroidal ring: same (radial, replica); section: same toroidal domain;
         // radial line: same (toroidal, replica)
-        NC(ncclCommSplit(c->world, c->rank_r * p->npartdom + c->rank_p, c->rank_t, &c->tor, nullptr));
-        NC(ncclCommSplit(c->world, c->rank_t, c->rank_r * p->npartdom + c->rank_p, &c->sect, nullptr));
-        NC(ncclCommSplit(c->world, c->rank_t * p->npartdom + c->rank_p, c->rank_r, &c->rad, nullptr));
+        NC(comm_split(c->world, c->rank_r * p->npartdom + c->rank_p, c->rank_t, &c->tor));
+        NC(comm_split(c->world, c->rank_t, c->rank_r * p->npartdom + c->rank_p, &c->sect));
+        NC(comm_split(c->world, c->rank_t * p->npartdom + c->rank_p, c->rank_r, &c->rad));
     }
     // shift buffers (movers per stage ~1% at 8 domains; allocate generously)
     if (p->ntoroidal > 1 || nrad > 1) {
@@ -523,6 +539,25 @@ extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, con
     return GTCP_OK;
 }
 
+extern "C" gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, const void* nccl_id,
+                                 void* cuda_stream, gtcp_ctx* out) {
+    return init_ctx(p, rank, nranks, nccl_id, nullptr, cuda_stream, out);
+}
+
+extern "C" gtcp_status gtcp_loopback_create(int nranks, void** hub) {
+    if (!hub || nranks < 1 || nranks > 16) return GTCP_EINVAL;
+    *hub = loop_hub_create(nranks);
+    return GTCP_OK;
+}
+
+extern "C" void gtcp_loopback_destroy(void* hub) { loop_hub_destroy(static_cast<LoopHub*>(hub)); }
+
+extern "C" gtcp_status gtcp_init_loopback(const gtcp_params* p, int rank, int nranks, void* hub, void* cuda_stream,
+                                          gtcp_ctx* out) {
+    if (!hub) return GTCP_EINVAL;
+    return init_ctx(p, rank, nranks, nullptr, static_cast<LoopHub*>(hub), cuda_stream, out);
+}
+
 extern "C" void gtcp_destroy(gtcp_ctx c) {
     if (!c) return;
     cudaStreamSynchronize(c->st);
@@ -541,12 +576,12 @@ extern "C" void gtcp_destroy(gtcp_ctx c) {
     F(c->d_counts);
     if (c->h_counts) cudaFreeHost(c->h_counts);
     if (c->h_dc) cudaFreeHost(c->h_dc);
+    if (c->h_nonfinite) cudaFreeHost(c->h_nonfinite);
     if (c->h_scalar) cudaFreeHost(c->h_scalar);
-    if (c->part) ncclCommDestroy(c->part);
-    if (c->sect) ncclCommDestroy(c->sect);
-    if (c->rad) ncclCommDestroy(c->rad);
-    if (c->tor) ncclCommDestroy(c->tor);
-    if (c->world) ncclCommDestroy(c->world);
+    comm_destroy(&c->sect);
+    comm_destroy(&c->rad);
+    comm_destroy(&c->tor);
+    comm_destroy(&c->world);
     delete c;
 }
 
@@ -590,6 +625,15 @@ static cudaError_t download_reals(gtcp_ctx c, double* host, const double* dev, l
     return cudaSuccess;
 }
 
+// a new particle state: clear the non-finite flag on the device and its host
+// mirror (after the stream drained, so no older flag copy lands afterwards)
+static cudaError_t reset_nonfinite(gtcp_ctx c) {
+    cudaError_t e = cudaMemsetAsync(&c->dc->nonfinite, 0, sizeof(int), c->st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
+    c->h_nonfinite[0] = 0;
+    return e;
+}
+
 // pointer to element `count` of a particle array of the context's element size
 static double* pofs(double* base, long long count) {
     return reinterpret_cast<double*>(reinterpret_cast<char*>(base) + count * (gtcp::g_prec32 ? 4 : 8));
@@ -626,12 +670,13 @@ static gtcp_status halo_exchange(gtcp_ctx c, double* H) {
     double* rb = c->halo_buf;  // [0]: from left (their P-1), [1..2]: from right (their 0, 1)
     // sends: left then right; receives: right then left -- with two domains
     // left == right and NCCL pairs same-peer messages in posting order.
-    NC(ncclGroupStart());
-    NC(ncclSend(p0, 2 * mg, ncclDouble, left, c->tor, c->st));
-    NC(ncclSend(H + (long long)P * mg, mg, ncclDouble, right, c->tor, c->st));
-    NC(ncclRecv(rb + mg, 2 * mg, ncclDouble, right, c->tor, c->st));
-    NC(ncclRecv(rb, mg, ncclDouble, left, c->tor, c->st));
-    NC(ncclGroupEnd());
+    long long* acct = &c->comm_bytes[c->cur_phase];
+    NC(comm_group_start());
+    NC(comm_send(c->tor, p0, 2 * mg, ncclDouble, left, c->st, acct));
+    NC(comm_send(c->tor, H + (long long)P * mg, mg, ncclDouble, right, c->st, acct));
+    NC(comm_recv(c->tor, rb + mg, 2 * mg, ncclDouble, right, c->st, acct));
+    NC(comm_recv(c->tor, rb, mg, ncclDouble, left, c->st, acct));
+    NC(comm_group_end());
     if (c->rank_t == 0) launch_seam_rotate(g, rb, pm1, -1, c->st);
     else CU(cudaMemcpyAsync(pm1, rb, mg * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
     if (c->rank_t == nt - 1) {
@@ -647,7 +692,7 @@ static gtcp_status halo_exchange(gtcp_ctx c, double* H) {
 // ----------------------------------------------------------------------------
 // charge
 // ----------------------------------------------------------------------------
-static bool g_unit_weight = false;  // marker-density deposit (w == 1)
+static thread_local bool g_unit_weight = false;  // marker-density deposit (w == 1)
 
 static gtcp_status deposit_fx(gtcp_ctx c) {
     const Geo& g = c->geo;
@@ -655,6 +700,13 @@ static gtcp_status deposit_fx(gtcp_ctx c) {
     if (g_unit_weight) {
         // w == 1: point the weight array at a constant-one buffer (scratch)
         s.x[4] = c->scratch;
+    }
+    if (c->nranks > 1 && !g_unit_weight) {
+        // one fixed-point scale F for every rank whose grids are summed (the
+        // ghost-plane merge, the section allreduce): F follows the GLOBAL
+        // max|w| (8 bytes; positive doubles order like their bit patterns)
+        NC(comm_allreduce(c->world, &c->dc->wmax_bits, &c->dc->wmax_bits, 1, ncclUint64, ncclMax, c->st,
+                          &c->comm_bytes[c->cur_phase]));
     }
     launch_fx_scale(c->dc, c->st);
     CU(cudaMemsetAsync(c->fx, 0, (size_t)(c->P + 1) * c->mgrid * sizeof(long long), c->st));
@@ -678,16 +730,18 @@ static gtcp_status charge_reduce(gtcp_ctx c) {
     if (c->prm.ntoroidal > 1) {
         int nt = c->prm.ntoroidal;
         int left = (c->rank_t - 1 + nt) % nt, right = (c->rank_t + 1) % nt;
-        NC(ncclGroupStart());
-        NC(ncclSend(c->fx + (long long)P * mg, mg, ncclInt64, right, c->tor, c->st));
-        NC(ncclRecv(c->fx_recv, mg, ncclInt64, left, c->tor, c->st));
-        NC(ncclGroupEnd());
+        long long* acct = &c->comm_bytes[c->cur_phase];
+        NC(comm_group_start());
+        NC(comm_send(c->tor, c->fx + (long long)P * mg, mg, ncclInt64, right, c->st, acct));
+        NC(comm_recv(c->tor, c->fx_recv, mg, ncclInt64, left, c->st, acct));
+        NC(comm_group_end());
         launch_rotate_add_i64(g, c->fx_recv, c->fx, c->rank_t == 0 ? +1 : 0, c->st);
     }
     if (c->prm.npartdom * c->prm.nradial > 1) {
         // particle replicas and radial domains of one toroidal domain hold partial
         // charges of the same (replicated) grid: exact int64 sum
-        NC(ncclAllReduce(c->fx, c->fx, (size_t)P * mg, ncclInt64, ncclSum, c->sect, c->st));
+        NC(comm_allreduce(c->sect, c->fx, c->fx, (size_t)P * mg, ncclInt64, ncclSum, c->st,
+                          &c->comm_bytes[c->cur_phase]));
     }
     launch_fx_to_real(g, c->fx, c->rhoH + mg, c->dc, P, c->st);
     launch_fill_dup(g, c->rhoH + mg, P, 1, c->st);
@@ -711,7 +765,9 @@ static gtcp_status compute_marker_norm(gtcp_ctx c) {
     s = charge_reduce(c);
     if (s != GTCP_OK) return s;
     launch_ring_sum(g, c->rhoH, c->ringsum, c->st);
-    if (c->prm.ntoroidal > 1) NC(ncclAllReduce(c->ringsum, c->ringsum, g.mpsi + 1, ncclDouble, ncclSum, c->tor, c->st));
+    if (c->prm.ntoroidal > 1)
+        NC(comm_allreduce(c->tor, c->ringsum, c->ringsum, g.mpsi + 1, ncclDouble, ncclSum, c->st,
+                          &c->comm_bytes[c->cur_phase]));
     launch_ring_mean(g, c->ringsum, c->nm, c->st);
     // restore max|w| of the real weights
     CU(cudaMemsetAsync(&c->dc->wmax_bits, 0, 8, c->st));
@@ -757,7 +813,9 @@ extern "C" gtcp_status gtcp_poisson_smooth(gtcp_ctx c) {
     gtcp_status s = smooth_H(c, c->dnH);
     if (s != GTCP_OK) return s;
     launch_ring_sum(g, c->dnH, c->ringsum, c->st);
-    if (c->prm.ntoroidal > 1) NC(ncclAllReduce(c->ringsum, c->ringsum, g.mpsi + 1, ncclDouble, ncclSum, c->tor, c->st));
+    if (c->prm.ntoroidal > 1)
+        NC(comm_allreduce(c->tor, c->ringsum, c->ringsum, g.mpsi + 1, ncclDouble, ncclSum, c->st,
+                          &c->comm_bytes[c->cur_phase]));
     launch_jacobi_init(g, c->dnH, c->ringsum, c->rhs, c->jphi, c->st);
     // the Poisson equation is 2-D per plane: the ranks of a section (radial
     // windows and particle replicas of one toroidal domain hold the same grid)
@@ -770,13 +828,13 @@ extern "C" gtcp_status gtcp_poisson_smooth(gtcp_ctx c) {
                            kb(s_me + 1) - kb(s_me), c->st);
     }
     if (S > 1) {
-        NC(ncclGroupStart());
+        NC(comm_group_start());
         for (int r = 0; r < S; r++) {
             double* bp = c->jphi + (long long)kb(r) * c->mgrid;
             const size_t cnt = (size_t)(kb(r + 1) - kb(r)) * c->mgrid;
-            if (cnt) NC(ncclBroadcast(bp, bp, cnt, ncclDouble, r, c->sect, c->st));
+            if (cnt) NC(comm_bcast(c->sect, bp, bp, cnt, ncclDouble, r, c->st, &c->comm_bytes[c->cur_phase]));
         }
-        NC(ncclGroupEnd());
+        NC(comm_group_end());
     }
     launch_zonal(g, c->ringsum, c->phi00, c->st);
     launch_add_zonal2(g, c->phi00, c->jphi, c->phiH, c->st);
@@ -838,6 +896,7 @@ extern "C" gtcp_status gtcp_push(gtcp_ctx c, int stage) {
         for (int d = 0; d < 5; d++) std::swap(c->live[d], c->saved[d]);
         c->stage_next = 1;
     }
+    CU(cudaMemcpyAsync(c->h_nonfinite, &c->dc->nonfinite, sizeof(int), cudaMemcpyDeviceToHost, c->st));
     KCHECK();
     return GTCP_OK;
 }
@@ -965,7 +1024,14 @@ extern "C" gtcp_status gtcp_step(gtcp_ctx c, int nsteps) {
             if ((r = gtcp_push(c, stage)) != GTCP_OK) return r;
             if ((r = gtcp_shift(c)) != GTCP_OK) return r;
         }
+        // the push raises a device flag on a non-finite state; its
+        // pinned mirror is refreshed after every push, checked here without
+        // waiting (a copy still in flight shows up one step later) ...
+        if (c->h_nonfinite[0]) return set_err(c, GTCP_ENONFINITE, "step: non-finite particle state");
     }
+    // ... and exactly once per call
+    CU(cudaStreamSynchronize(c->st));
+    if (c->h_nonfinite[0]) return set_err(c, GTCP_ENONFINITE, "step: non-finite particle state");
     return GTCP_OK;
 }
 
@@ -1000,6 +1066,7 @@ extern "C" gtcp_status gtcp_load(gtcp_ctx c) {
                           std::min<long long>(c->rank_p, n_rad % p.npartdom);
     c->n = n;
     c->stage_next = 1;
+    CU(reset_nonfinite(c));
     PSet s = live_set(c);
     const double zlo = c->k0 * (GTCP_TWO_PI / p.mzetamax), zhi = (c->k0 + c->P) * (GTCP_TWO_PI / p.mzetamax);
     const double rlo = p.a0 + c->rad_ring[c->rank_r] * dr;
@@ -1026,6 +1093,7 @@ extern "C" gtcp_status gtcp_set_particles(gtcp_ctx c, int64_t n, const double* c
     if (c->id && id) CU(cudaMemcpyAsync(c->id, id, n * sizeof(uint64_t), cudaMemcpyHostToDevice, c->st));
     c->n = n;
     c->stage_next = 1;
+    CU(reset_nonfinite(c));
     gtcp_status r = do_bin(c);
     if (r != GTCP_OK) return r;
     r = compute_marker_norm(c);
@@ -1072,8 +1140,8 @@ extern "C" gtcp_status gtcp_sample_particles(gtcp_ctx c, int64_t m, const int64_
         CU(cudaMemcpyAsync(attr[d], d_out, m * sizeof(double), cudaMemcpyDeviceToHost, c->st));
     }
     if (id && c->id) {
-        launch_gather_f64((const double*)c->id, d_idx, m, d_out, c->st);
-        CU(cudaMemcpyAsync(id, d_out, m * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+        launch_gather_u64(c->id, d_idx, m, reinterpret_cast<unsigned long long*>(d_out), c->st);
+        CU(cudaMemcpyAsync(id, d_out, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
     }
     CU(cudaFreeAsync(d_idx, c->st));
     CU(cudaFreeAsync(d_out, c->st));
@@ -1082,19 +1150,30 @@ extern "C" gtcp_status gtcp_sample_particles(gtcp_ctx c, int64_t m, const int64_
     return GTCP_OK;
 }
 
-extern "C" gtcp_status gtcp_step_host(gtcp_ctx c, int64_t n, double* const* attr, int nsteps) {
+extern "C" gtcp_status gtcp_step_host(gtcp_ctx c, int64_t n, int64_t cap, double* const* attr, int nsteps,
+                                      int64_t* n_out) {
     CHECK_CTX(c);
-    if (n < 0 || n > c->cap || !attr) return set_err(c, GTCP_EINVAL, "step_host: bad args");
+    if (n < 0 || n > c->cap || cap < 0 || !attr || !n_out) return set_err(c, GTCP_EINVAL, "step_host: bad args");
     for (int d = 0; d < 6; d++)
         if (!attr[d]) return set_err(c, GTCP_EINVAL, "step_host: null attribute");
     for (int d = 0; d < 5; d++) CU(upload_reals(c, c->live[d], attr[d], n));
     CU(upload_reals(c, c->mu, attr[5], n));
     c->n = n;
     c->stage_next = 1;
+    // the tiles of the last bin stay: they are exact for a state returned by
+    // the previous step_host (same order); for any other order the deposit's
+    // out-of-window path keeps the charge exact (slower)
+    c->n_binned = std::min<long long>(c->n_binned, n);
+    CU(reset_nonfinite(c));
+    CU(cudaMemsetAsync(&c->dc->wmax_bits, 0, 8, c->st));
     launch_wmax(c->live[4], c->n, c->dc, c->st);
     gtcp_status r = gtcp_step(c, nsteps);
     if (r != GTCP_OK) return r;
+    *n_out = c->n;
+    if (c->n > cap) return set_err(c, GTCP_ECAPACITY, "step_host: owned count exceeds cap");
+    // live state and mu: a bin or a shift inside the steps reorders them together
     for (int d = 0; d < 5; d++) CU(download_reals(c, attr[d], c->live[d], c->n));
+    CU(download_reals(c, attr[5], c->mu, c->n));
     CU(cudaStreamSynchronize(c->st));
     return GTCP_OK;
 }
@@ -1181,8 +1260,8 @@ extern "C" gtcp_status gtcp_stats(gtcp_ctx c, gtcp_stats_t* out) {
     long long nl = c->n;
     CU(cudaMemcpyAsync(c->d_scalar + 1, &nl, 8, cudaMemcpyHostToDevice, c->st));
     if (c->nranks > 1) {
-        NC(ncclAllReduce(c->d_scalar, c->d_scalar + 2, 1, ncclDouble, ncclSum, c->world, c->st));
-        NC(ncclAllReduce(c->d_scalar + 1, c->d_scalar + 3, 1, ncclInt64, ncclSum, c->world, c->st));
+        NC(comm_allreduce(c->world, c->d_scalar, c->d_scalar + 2, 1, ncclDouble, ncclSum, c->st, nullptr));
+        NC(comm_allreduce(c->world, c->d_scalar + 1, c->d_scalar + 3, 1, ncclInt64, ncclSum, c->st, nullptr));
     } else {
         CU(cudaMemcpyAsync(c->d_scalar + 2, c->d_scalar, 16, cudaMemcpyDeviceToDevice, c->st));
     }
@@ -1218,6 +1297,7 @@ extern "C" gtcp_status gtcp_timings(gtcp_ctx c, gtcp_timings_t* out) {
         out->calls[i] = c->t_calls[i];
     }
     out->launches = gtcp::g_launches - c->launches0;
+    for (int i = 0; i < GTCP_NPHASE; i++) out->comm_bytes[i] = c->comm_bytes[i];
     return GTCP_OK;
 }
 
@@ -1225,7 +1305,7 @@ extern "C" gtcp_status gtcp_timings_reset(gtcp_ctx c) {
     CHECK_CTX(c);
     CU(cudaStreamSynchronize(c->st));
     fold_pending(c);
-    for (int i = 0; i < GTCP_NPHASE; i++) { c->t_ms[i] = 0; c->t_calls[i] = 0; }
+    for (int i = 0; i < GTCP_NPHASE; i++) { c->t_ms[i] = 0; c->t_calls[i] = 0; c->comm_bytes[i] = 0; }
     c->launches0 = gtcp::g_launches;
     return GTCP_OK;
 }
@@ -1262,13 +1342,17 @@ gtcp_status shift_exchange(gtcp_ctx c, int dir) {
     // dir 0: toroidal ring (periodic); dir 1: radial line (inner = left, outer = right)
     const int nt = dir ? c->prm.nradial : c->prm.ntoroidal;
     const int me = dir ? c->rank_r : c->rank_t;
-    ncclComm_t comm = dir ? c->rad : c->tor;
+    const Comm& comm = dir ? c->rad : c->tor;
+    long long* acct = &c->comm_bytes[c->cur_phase];
     const int left = dir ? (me > 0 ? me - 1 : -1) : (me - 1 + nt) % nt;
     const int right = dir ? (me < nt - 1 ? me + 1 : -1) : (me + 1) % nt;
     // movers carry the live state and mu, plus the saved RK2 state mid-step (H-3)
     const int nattr = (c->stage_next == 2) ? 11 : 6;
     long long start = 0;  // first pass scans everything, later passes only the arrivals
-    for (int iter = 0; iter <= nt; iter++) {
+    bool settled = false;
+    // multi-hop guard: a particle crosses at most nt domains in one
+    // shift, so pass nt + 1 must find no movers
+    for (int iter = 0; iter <= nt + 1; iter++) {
         double* attrs[11];
         for (int d = 0; d < 5; d++) attrs[d] = pofs(c->live[d], start);
         attrs[5] = pofs(c->mu, start);
@@ -1296,20 +1380,24 @@ gtcp_status shift_exchange(gtcp_ctx c, int dir) {
         if (iter == 0) mark();
         // counts: mine (left, right) out; theirs in; global mover total
         CU(cudaMemsetAsync(c->d_counts + 2, 0, 2 * sizeof(long long), c->st));
-        NC(ncclGroupStart());
-        if (left >= 0) NC(ncclSend(c->d_counts + 0, 1, ncclInt64, left, comm, c->st));
-        if (right >= 0) NC(ncclSend(c->d_counts + 1, 1, ncclInt64, right, comm, c->st));
-        if (right >= 0) NC(ncclRecv(c->d_counts + 2, 1, ncclInt64, right, comm, c->st));  // right's left-movers
-        if (left >= 0) NC(ncclRecv(c->d_counts + 3, 1, ncclInt64, left, comm, c->st));    // left's right-movers
-        NC(ncclGroupEnd());
+        NC(comm_group_start());
+        if (left >= 0) NC(comm_send(comm, c->d_counts + 0, 1, ncclInt64, left, c->st, acct));
+        if (right >= 0) NC(comm_send(comm, c->d_counts + 1, 1, ncclInt64, right, c->st, acct));
+        if (right >= 0) NC(comm_recv(comm, c->d_counts + 2, 1, ncclInt64, right, c->st, acct));  // right's left-movers
+        if (left >= 0) NC(comm_recv(comm, c->d_counts + 3, 1, ncclInt64, left, c->st, acct));    // left's right-movers
+        NC(comm_group_end());
         launch_sum_i64_pair(c->d_counts, c->d_counts + 4, c->st);
-        NC(ncclAllReduce(c->d_counts + 4, c->d_counts + 5, 1, ncclInt64, ncclSum, comm, c->st));
+        NC(comm_allreduce(comm, c->d_counts + 4, c->d_counts + 5, 1, ncclInt64, ncclSum, c->st, acct));
         CU(cudaMemcpyAsync(c->h_counts, c->d_counts, 6 * sizeof(long long), cudaMemcpyDeviceToHost, c->st));
         if (iter == 0) mark();
         CU(cudaStreamSynchronize(c->st));
         const long long nL = c->h_counts[0], nR = c->h_counts[1], rR = c->h_counts[2], rL = c->h_counts[3];
         const long long total = c->h_counts[5];
-        if (total == 0) break;
+        if (total == 0) {
+            settled = true;
+            break;
+        }
+        if (iter == nt + 1) break;
         if (nL > c->shift_cap || nR > c->shift_cap)
             return set_err(c, GTCP_ECAPACITY, "shift: send buffer overflow");
         const long long nkeep = n - nL - nR;
@@ -1330,32 +1418,30 @@ gtcp_status shift_exchange(gtcp_ctx c, int dir) {
         KCHECK();
         if (iter == 0) mark();
         // payload: straight into the particle arrays behind the keepers
-        NC(ncclGroupStart());
+        NC(comm_group_start());
         for (int d = 0; d < nattr; d++) {
             const ncclDataType_t ty = g.prec32 ? ncclFloat : ncclDouble;
-            if (left >= 0) NC(ncclSend(c->sendL[d], nL, ty, left, comm, c->st));
-            if (right >= 0) NC(ncclSend(c->sendR[d], nR, ty, right, comm, c->st));
-            if (right >= 0) NC(ncclRecv(pofs(attrs[d], nkeep), rR, ty, right, comm, c->st));
-            if (left >= 0) NC(ncclRecv(pofs(attrs[d], nkeep + rR), rL, ty, left, comm, c->st));
+            if (left >= 0) NC(comm_send(comm, c->sendL[d], nL, ty, left, c->st, acct));
+            if (right >= 0) NC(comm_send(comm, c->sendR[d], nR, ty, right, c->st, acct));
+            if (right >= 0) NC(comm_recv(comm, pofs(attrs[d], nkeep), rR, ty, right, c->st, acct));
+            if (left >= 0) NC(comm_recv(comm, pofs(attrs[d], nkeep + rR), rL, ty, left, c->st, acct));
         }
         if (idp) {
-            if (left >= 0) NC(ncclSend(c->sidL, nL, ncclUint64, left, comm, c->st));
-            if (right >= 0) NC(ncclSend(c->sidR, nR, ncclUint64, right, comm, c->st));
-            if (right >= 0) NC(ncclRecv(idp + nkeep, rR, ncclUint64, right, comm, c->st));
-            if (left >= 0) NC(ncclRecv(idp + nkeep + rR, rL, ncclUint64, left, comm, c->st));
+            if (left >= 0) NC(comm_send(comm, c->sidL, nL, ncclUint64, left, c->st, acct));
+            if (right >= 0) NC(comm_send(comm, c->sidR, nR, ncclUint64, right, c->st, acct));
+            if (right >= 0) NC(comm_recv(comm, idp + nkeep, rR, ncclUint64, right, c->st, acct));
+            if (left >= 0) NC(comm_recv(comm, idp + nkeep + rR, rL, ncclUint64, left, c->st, acct));
         }
-        NC(ncclGroupEnd());
+        NC(comm_group_end());
         if (iter == 0) mark();
         c->movers_sent += nL + nR;
         c->movers_recv += rL + rR;
         c->n = start + nkeep + rL + rR;
         start = start + nkeep;  // only the arrivals can still be misplaced
     }
-    mark();
-    // the fixed-point charge scale needs a bound on max|w| of the new particle
-    // set: the max over the toroidal ranks is one (positive doubles order like
-    // their uint64 bit patterns), no pass over the weights needed
-    NC(ncclAllReduce(&c->dc->wmax_bits, &c->dc->wmax_bits, 1, ncclUint64, ncclMax, comm, c->st));
+    if (!settled) return set_err(c, GTCP_EINVARIANT, "shift: movers left after the multi-hop guard");
+    // (the fixed-point charge scale needs max|w| of the new particle set: the
+    // next deposit takes the max over all ranks, which bounds the arrivals too)
     mark();
     KCHECK();
     if (prof) {

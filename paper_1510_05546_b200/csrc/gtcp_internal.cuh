@@ -5,10 +5,13 @@
 #include <nccl.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include <string>
 #include <vector>
 
 #include "../../include/gtcp.h"
+#include "gtcp_comm.cuh"
 
 #define GTCP_TWO_PI (2.0 * 3.14159265358979323846)
 
@@ -161,8 +164,10 @@ void launch_shift_backfill(double* const* attrs, int nattr, unsigned long long* 
                            unsigned* holes, unsigned* fills, long long nholes, cudaStream_t st);
 void launch_fill_f64(double* x, long long n, double v, cudaStream_t st);
 void launch_gather_f64(const double* src, const long long* idx, long long m, double* out, cudaStream_t st);
+void launch_gather_u64(const unsigned long long* src, const long long* idx, long long m, unsigned long long* out,
+                       cudaStream_t st);
 
-extern long long g_launches;  // kernels launched (for the bench's gpu_launches claim)
-extern int g_prec32;          // precision of the current context's particle store
+extern std::atomic<long long> g_launches;  // kernels launched (for the bench's gpu_launches claim)
+extern thread_local int g_prec32;         // precision of the current context's particle store
 
 }  // namespace gtcp

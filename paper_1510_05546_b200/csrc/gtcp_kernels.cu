@@ -30,8 +30,8 @@
 
 namespace gtcp {
 
-long long g_launches = 0;
-int g_prec32 = 0;  // precision of the particle store of the context being driven (set per call)
+std::atomic<long long> g_launches{0};
+thread_local int g_prec32 = 0;  // precision of the particle store of the context being driven (set per call)
 
 static constexpr double kInvTwoPi = 1.0 / GTCP_TWO_PI;
 static constexpr double kInvPi = 2.0 / GTCP_TWO_PI;
@@ -62,13 +62,32 @@ __device__ __forceinline__ long long fx_round(double a, double b) {
     return __double_as_longlong(t) - __double_as_longlong(M);
 }
 
+// floor of x (|x| < 2^51) with fp64 adds only: x + 1.5*2^52 rounded toward
+// -inf is exactly 1.5*2^52 + floor(x), whose low word is the integer; the
+// difference is floor(x) as a double.  Bitwise the same as floor() and a
+// (double)(int) round trip, without the F2I / I2F / FRND conversions whose
+// variable latency stalls the issue on the short scoreboard.  Callers make
+// sure x is finite (the deposit skips non-finite markers; the push flags them).
+__device__ __forceinline__ double floor_fx(double x, int* i) {
+    const double M = 6755399441055744.0;
+    const double t = __dadd_rd(x, M);
+    *i = __double2loint(t);
+    return __dsub_rn(t, M);
+}
+// (double)i for 0 <= i < 2^31, the same way round: the bits of 1.5*2^52 + i
+// minus the constant (exact)
+__device__ __forceinline__ double i2d_fx(int i) {
+    return __dsub_rn(__hiloint2double(0x43380000, i), 6755399441055744.0);
+}
+
 // Q-2 / H-1: global plane interval and its upper weight.  Same operation
 // sequence as the oracle (single rounded multiply, floor), bit-exact.
 __device__ __forceinline__ int plane_of(const Geo& g, double zeta, double* wz1) {
     double tg = __dmul_rn(zeta, g.cz);
-    int k = (int)floor(tg);
+    int k;
+    floor_fx(tg, &k);
     k = min(max(k, 0), g.mzetamax - 1);
-    *wz1 = __dsub_rn(tg, (double)k);
+    *wz1 = __dsub_rn(tg, i2d_fx(k));
     return k;
 }
 
@@ -89,19 +108,23 @@ __device__ __forceinline__ void gyro_stencil(const Geo& g, double r, double thet
         if (l == 3) tl = __dsub_rn(theta, rho_r);
         rl = fmin(fmax(rl, g.a0), g.a1);
         double x = __dmul_rn(__dsub_rn(rl, g.a0), g.inv_dr);
-        int i = (int)floor(x);
+        int i;
+        floor_fx(x, &i);
         i = min(max(i, 0), g.mpsi - 1);
-        double wp1 = __dsub_rn(x, (double)i);
+        double wp1 = __dsub_rn(x, i2d_fx(i));
 #pragma unroll
         for (int mm = 0; mm < 2; mm++) {
             int m = i + mm;
             double qt = __ldg(g.qtinv + m);
             int mt = __ldg(g.mtheta + m);
             double s = __dmul_rn(__fma_rn(-zeta, qt, tl), kInvTwoPi);
-            s = __dsub_rn(s, floor(s));
+            int jw;
+            s = __dsub_rn(s, floor_fx(s, &jw));
             s = __dmul_rn(s, (double)mt);
-            int j = min((int)floor(s), mt - 1);
-            double wt1 = __dsub_rn(s, (double)j);
+            int j;
+            floor_fx(s, &j);
+            j = (int)min((unsigned)j, (unsigned)(mt - 1));
+            double wt1 = __dsub_rn(s, i2d_fx(j));
             double wp = mm ? wp1 : __dsub_rn(1.0, wp1);
             fn(m, j, mt, __dmul_rn(__dmul_rn(0.25, wp), __dsub_rn(1.0, wt1)), __dmul_rn(__dmul_rn(0.25, wp), wt1));
         }
@@ -204,6 +227,7 @@ __global__ void __launch_bounds__(256) k_deposit_direct(Geo g, PSet s, long long
          p += (long long)gridDim.x * blockDim.x) {
         double psi = ldp<R>(s.x[0], p), theta = ldp<R>(s.x[1], p), zeta = ldp<R>(s.x[2], p), w = ldp<R>(s.x[4], p),
                mu = ldp<R>(s.mu, p);
+        if (!isfinite((psi + theta + zeta + mu) * 0.0 + w)) continue;  // flagged by the push; never deposited
         double r, invB, rho, inv_r;
         gyro_radius(g, psi, cos_theta(theta), mu, &r, &invB, &rho, &inv_r);
         double wz1;
@@ -465,6 +489,8 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
                 n_psi = ldp_cs<R>(s.x[0], pn); n_theta = ldp_cs<R>(s.x[1], pn); n_zeta = ldp_cs<R>(s.x[2], pn);
                 n_w = ldp_cs<R>(s.x[4], pn); n_mu = ldp_cs<R>(s.mu, pn);
             }
+            // a non-finite marker (flagged by the push) is never deposited
+            if (!isfinite((psi + theta + zeta + mu) * 0.0 + w)) continue;
             double r, invB, rho, inv_r;
             gyro_radius(g, psi, cos_theta(theta), mu, &r, &invB, &rho, &inv_r);
             double wz1;
@@ -492,8 +518,10 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
                 const double tl2 = __fma_rn(stt, rho_r, theta);
                 rl = fmin(fmax(rl, g.a0), g.a1);
                 const double x = __dmul_rn(__dsub_rn(rl, g.a0), g.inv_dr);
-                const int ir = min(max((int)floor(x), 0), g.mpsi - 1);
-                const double wp1 = __dsub_rn(x, (double)ir);
+                int ir;
+                floor_fx(x, &ir);
+                ir = min(max(ir, 0), g.mpsi - 1);
+                const double wp1 = __dsub_rn(x, i2d_fx(ir));
                 // both rings' table entries and window rows are fetched before
                 // any use, so the shared-memory latency overlaps the arithmetic
                 int qcs[2];
@@ -512,10 +540,13 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
                     const int mm = mq ^ b2;  // lane-rotated ring choice
                     const RingT rt = rts[mq];
                     double sl = __dmul_rn(__fma_rn(-zeta, rt.qt, tl2), kInvTwoPi);
-                    sl = __dsub_rn(sl, floor(sl));
+                    int jw;
+                    sl = __dsub_rn(sl, floor_fx(sl, &jw));
                     sl = __dmul_rn(sl, rt.mtd);
-                    const int j = min((int)floor(sl), rt.mt - 1);
-                    const double wt1 = __dsub_rn(sl, (double)j);
+                    int j;
+                    floor_fx(sl, &j);
+                    j = (int)min((unsigned)j, (unsigned)(rt.mt - 1));
+                    const double wt1 = __dsub_rn(sl, i2d_fx(j));
                     // wp = mm ? wp1 : 1 - wp1, and the node weights rotated by lane
                     // bit 4, each as one exact fma(+-1, x, {0, 1})
                     const double sm = mm ? 1.0 : -1.0, s4 = b4 ? 1.0 : -1.0;
@@ -790,16 +821,21 @@ __device__ __forceinline__ void push_one(const Geo& g, const RingTab* __restrict
             if (l == 3) tl = theta - rho_r;
             rl = fmin(fmax(rl, g.a0), g.a1);
             const double x = (rl - g.a0) * g.inv_dr;
-            const int i = min(max((int)floor(x), 0), g.mpsi - 1);
-            const double wp1 = x - (double)i;
+            int i;
+            floor_fx(x, &i);
+            i = min(max(i, 0), g.mpsi - 1);
+            const double wp1 = x - i2d_fx(i);
 #pragma unroll
             for (int mm = 0; mm < 2; mm++) {
                 const RingTab t = rt[i + mm];
                 double s = (tl - zeta * t.qtinv) * kInvTwoPi;
-                s = s - floor(s);
+                int jw;
+                s = s - floor_fx(s, &jw);
                 s = s * (double)t.mtheta;
-                const int j = min((int)floor(s), t.mtheta - 1);
-                const double wt1 = s - (double)j;
+                int j;
+                floor_fx(s, &j);
+                j = (int)min((unsigned)j, (unsigned)(t.mtheta - 1));
+                const double wt1 = s - i2d_fx(j);
                 const double wp = mm ? wp1 : 1.0 - wp1;
                 node[2 * l + mm] = t.igrid + j;
                 wa[2 * l + mm] = wp * (1.0 - wt1);
@@ -1415,6 +1451,20 @@ void launch_gather_f64(const double* src, const long long* idx, long long m, dou
     int blocks = (int)std::max<long long>(1, std::min<long long>((m + 255) / 256, 148LL * 8));
     if (g_prec32) k_gather_f64<float><<<blocks, 256, 0, st>>>(src, idx, m, out);
     else k_gather_f64<double><<<blocks, 256, 0, st>>>(src, idx, m, out);
+    g_launches++;
+}
+
+// 8-byte ids: always 64-bit elements, whatever the particle store precision
+__global__ void k_gather_u64(const unsigned long long* __restrict__ src, const long long* __restrict__ idx, long long m,
+                             unsigned long long* __restrict__ out) {
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < m; q += (long long)gridDim.x * blockDim.x)
+        out[q] = src[idx[q]];
+}
+
+void launch_gather_u64(const unsigned long long* src, const long long* idx, long long m, unsigned long long* out,
+                       cudaStream_t st) {
+    int blocks = (int)std::max<long long>(1, std::min<long long>((m + 255) / 256, 148LL * 8));
+    k_gather_u64<<<blocks, 256, 0, st>>>(src, idx, m, out);
     g_launches++;
 }
 

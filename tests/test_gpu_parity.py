@@ -315,7 +315,7 @@ def test_toroidal_decomposition_parity_2gpu(G, args):
         pytest.skip("needs 2 GPUs")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "tools", "dist_parity.py")] + args
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "tests", "dist_parity.py")] + args
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert '"ok": true' in r.stdout

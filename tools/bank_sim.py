@@ -15,7 +15,7 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import oracle  # noqa: E402
+import paper_1510_05546_b200 as G  # noqa: E402  (host geometry only; no GPU needed)
 import synth  # noqa: E402
 
 TWO_PI = 2 * math.pi
@@ -24,10 +24,10 @@ TWO_PI = 2 * math.pi
 def build(size, mzetamax, ring_frac, tile_max, nmu, seed, layout):
     over = {"mzetamax": mzetamax} if mzetamax else {}
     cfg = synth.config(size, **over)
-    p = oracle.make_params(cfg)
-    g = oracle.geometry(p)
+    p = G.gtcp_default_params(size, **over)
+    g = G.gtcp_geometry(p)
     M, P = p.mpsi, p.mzetamax
-    mt, ig, qt = np.array(g.mtheta), np.array(g.igrid), np.array(g.qtinv)
+    mt, ig, qt = np.array(g["mtheta"]), np.array(g["igrid"]), np.array(g["qtinv"])
     a0, a1 = p.a0, p.a1
     dr = (a1 - a0) / M
     om = p.omega0
