@@ -287,6 +287,19 @@ def run_gpu(args):
             roof[name] = {"avg_ms": avg_ms, "achieved_gbs": gbs, "frac": gbs / hbm,
                           "bytes_per_particle": nbytes, "share_of_step": ms_tot / max(ms, 1e-9)}
     dom = max(roof, key=lambda k: roof[k]["share_of_step"]) if roof else None
+    # inter-GPU bytes the library moved per phase (NCCL bus-byte convention,
+    # counted in libgtcp), over that phase's event time: a lower bound of the
+    # link rate, since each phase also holds the kernels around its collectives
+    comm = {}
+    for ph in ("charge", "charge_red", "poisson", "shift"):
+        b = tm.get(f"{ph}_comm_bytes", 0)
+        if b:
+            t_ms = tm[f"{ph}_ms"]
+            comm[ph] = {"bytes_per_step": b / args.steps, "ms_per_step": t_ms / args.steps,
+                        "gbs_over_phase": b / (t_ms * 1e-3) / 1e9 if t_ms else None}
+    if comm:
+        comm["nvlink_ref_gbs"] = {"peer_copy_per_direction": 770, "nominal_per_direction": 900,
+                                  "source": "/opt/skills/guides/B200_PROFILING.md (measured on this pool)"}
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
@@ -344,12 +357,12 @@ def run_gpu(args):
         cpu = None
         if world == 1 and not args.no_cpu:
             v, dt, nthr = cpu_baseline(size, args.ref_sample, 1, parallel=True)
-            v1, dt1, _ = cpu_baseline(size, args.ref_sample // 4, 1, parallel=False)
+            v1, dt1, _ = cpu_baseline(size, args.ref_sample // 8, 1, parallel=False)
             cpu = {"value": v, "unit": UNIT, "cores": nthr, "kind": "oracle",
                    "sample": f"{args.ref_sample} markers of class {size} on its full grid, one step of "
                              f"charge+push+shift with a fixed field ({dt:.1f} s on {nthr} OpenMP threads, "
                              f"per-thread grid replicas summed in a fixed order, P:330)",
-                   "single_thread": {"value": v1, "sample": f"{args.ref_sample // 4} markers, {dt1:.1f} s"},
+                   "single_thread": {"value": v1, "sample": f"{args.ref_sample // 8} markers, {dt1:.1f} s"},
                    "host": host_info()}
         r = roof.get(dom, {})
         out = {
@@ -368,6 +381,8 @@ def run_gpu(args):
                          "all": roof},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
         }
+        if world > 1:
+            out["comm"] = comm
         print(json.dumps(out), flush=True)
     ctx.close()
     if dist:
@@ -383,7 +398,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--size", default=None)
     ap.add_argument("--bin-every", type=int, default=2)
-    ap.add_argument("--ref-sample", type=int, default=4_000_000)
+    ap.add_argument("--ref-sample", type=int, default=16_000_000)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -483,7 +483,7 @@ static gtcp_status init_ctx(const gtcp_params* p, int rank, int nranks, const vo
     c->dep_smem = gtcp::deposit_tiled_smem(P, c->dep_nb);
     if (c->dep_smem > (size_t)smem_optin) c->dep_cap_nodes = 0;
     c->dep_ctas = nsm * c->dep_nb;
-    if (P + 1 > 80 || c->dep_cap_nodes < 1024) {
+    if (P + 1 > 80 || c->dep_cap_nodes < 1024 || p->mthetamax >= 8192) {  // packed rows: labels < 2^13
         c->charge_mode = 1;
     } else {
         CU(configure_deposit_tiled(c->dep_smem, c->dep_nb));
@@ -701,6 +701,7 @@ static gtcp_status deposit_fx(gtcp_ctx c) {
         // w == 1: point the weight array at a constant-one buffer (scratch)
         s.x[4] = c->scratch;
     }
+#ifndef GTCP_NO_FX_AGREE  // (defined only in the regression-demonstration build of tools/fx_agree_demo.sh)
     if (c->nranks > 1 && !g_unit_weight) {
         // one fixed-point scale F for every rank whose grids are summed (the
         // ghost-plane merge, the section allreduce): F follows the GLOBAL
@@ -708,6 +709,7 @@ static gtcp_status deposit_fx(gtcp_ctx c) {
         NC(comm_allreduce(c->world, &c->dc->wmax_bits, &c->dc->wmax_bits, 1, ncclUint64, ncclMax, c->st,
                           &c->comm_bytes[c->cur_phase]));
     }
+#endif
     launch_fx_scale(c->dc, c->st);
     CU(cudaMemsetAsync(c->fx, 0, (size_t)(c->P + 1) * c->mgrid * sizeof(long long), c->st));
     long long tiled_end = 0;

@@ -310,10 +310,9 @@ struct WinTables {
 
 // per-ring constants of the tile band (index nr = the "outside the band" ring:
 // W = 0, so every contribution lands in the trash slot and is redone via L2)
-struct RingT {
-    double qt, mtd;
+struct RingT {  // 16 bytes: one LDS.128 per (gyro-point, ring)
+    double qt;
     int mt, W;
-    int pad0, pad1;
 };
 
 // limbs of the fixed-point value v = round(a*b) taken straight from the bits of
@@ -337,9 +336,18 @@ __device__ __forceinline__ unsigned wrap_diff(int j, int js, int mt) {
 
 // Shared-memory layout of k_deposit_tiled (dynamic): low limbs [kDepCap + 1]
 // (index kDepCap = trash slot), high limbs at the fixed distance kDepStride
-// (an immediate offset in the ATOMS), row table [(P+1) x kRowStride] of
-// (label window start, byte offset of the row), column -> ring bytes.
-static constexpr int kRowStride = kMaxRings + 1;
+// (an immediate offset in the ATOMS), interval row table [P x kITStride] of
+// int2 = (row of plane k, row of plane k + 1) for plane interval k and ring
+// q, column -> ring bytes.  A row packs the label window start (bits 0..12)
+// and the word offset of the window row (bits 13..31), so one LDS.64 gives a
+// marker both of its planes' rows: the table lookups were ~36 % of the
+// L1/shared data-pipe wavefronts that bound this kernel (ncu, r02).
+// kITStride = 24 entries (48 banks = 16 mod 32 per interval): the rows of
+// intervals k and k+1 for rings q and q+1 never share a bank.
+static constexpr int kITStride = 24;
+static constexpr int kRowXBits = 13;  // label window start < 8192 (mthetamax < 8192, checked at init)
+__device__ __forceinline__ int row_x(int row) { return row & ((1 << kRowXBits) - 1); }
+__device__ __forceinline__ int row_y(int row) { return (int)((unsigned)row >> kRowXBits) << 2; }  // byte offset
 #ifdef GTCP_DUMP_ADDR
 // debug build only: word offsets of the lo-limb ATOMS of the first 8 iterations
 // of the 8 warps of 64 tiles spread over the launch ([tile][iter][warp][32][32])
@@ -358,10 +366,10 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     unsigned* slo = reinterpret_cast<unsigned*>(smem_raw);
     int* shi = reinterpret_cast<int*>(slo + kDepStride);
-    int2* rowt = reinterpret_cast<int2*>(slo + 2 * kDepStride);  // 8-byte aligned: 2*kDepStride is even
-    unsigned char* colq = reinterpret_cast<unsigned char*>(rowt + (g.P + 1) * kRowStride);  // [S] ring of column
+    int2* itab = reinterpret_cast<int2*>(slo + 2 * kDepStride);  // 8-byte aligned: 2*kDepStride is even
+    unsigned char* colq = reinterpret_cast<unsigned char*>(itab + g.P * kITStride);  // [S] ring of column
     __shared__ WinTables T;
-    __shared__ RingT RT[kMaxRings + 1];
+    __shared__ __align__(16) RingT RT[kMaxRings + 1];
     __shared__ unsigned long long s_fallback;
     const double scale = fx_scale(dc);
     const int ntiles = *ntiles_p;
@@ -418,9 +426,9 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
             const int mti = __ldg(g.mtheta + i);
             const double fc = 0.5 * (double)(tl.c0 + tl.c1 + 1) / mti;
             const int nr = T.nr, S = T.S;
-            for (int e = threadIdx.x; e < P1 * kRowStride; e += blockDim.x) {
-                int kk = e / kRowStride, q = e - kk * kRowStride;
-                int2 row = make_int2(0, 4 * kDepCap);  // outside the band: trash slot
+            // packed row of plane kk, ring q: (label window start, word offset);
+            // outside the band or without a window: the trash slot
+            auto row_of = [&](int kk, int q) -> int {
                 if (q < nr && S > 0) {
                     int m = T.m_lo + q;
                     int mt = T.mt[q];
@@ -429,12 +437,14 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
                     double zk = (double)(g.k0 + kk) * g.dzeta;
                     double f = fc + zk * dq - hw;
                     f = f - floor(f);
-                    row.x = min(max((int)floor(f * mt), 0), mt - 1);
-                    row.y = 4 * (kk * S + T.WO[q].y);
-                } else if (q < nr) {
-                    row = make_int2(0, 4 * kDepCap);  // no window: W = 0 sends everything to the trash slot
+                    const int x = min(max((int)floor(f * mt), 0), mt - 1);
+                    return x | ((kk * S + T.WO[q].y) << kRowXBits);
                 }
-                rowt[e] = row;
+                return kDepCap << kRowXBits;
+            };
+            for (int e = threadIdx.x; e < g.P * kITStride; e += blockDim.x) {
+                const int k = e / kITStride, q = e - k * kITStride;
+                itab[e] = make_int2(row_of(k, q), row_of(k + 1, q));
             }
             if (threadIdx.x <= kMaxRings) {
                 const int q = threadIdx.x;
@@ -443,15 +453,12 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
                     const int m = T.m_lo + q;
                     rt.qt = __ldg(g.qtinv + m);
                     rt.mt = T.mt[q];
-                    rt.mtd = (double)rt.mt;
                     rt.W = T.WO[q].x;
                 } else {
                     rt.qt = 0.0;
                     rt.mt = 1;
-                    rt.mtd = 1.0;
                     rt.W = 0;
                 }
-                rt.pad0 = rt.pad1 = 0;
                 RT[q] = rt;
             }
             for (int x = threadIdx.x; x < S; x += blockDim.x) colq[x] = 0xFF;  // trash / padding columns
@@ -503,8 +510,7 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
             // lane-rotated plane order, fixed for the whole particle: pass A uses
             // plane k + b3, pass B plane k + 1 - b3
             const double wzA = b3 ? wzu : wzl, wzB = b3 ? wzl : wzu;
-            const int2* rowA = rowt + (k + b3) * kRowStride;
-            const int2* rowB = rowt + (k + 1 - b3) * kRowStride;
+            const int2* itk = itab + k * kITStride;  // rows of planes k, k + 1 (pass A = plane k + b3)
             int bad = -1;  // max over contributions of (window offset - W): >= 0 iff one hit a trash column
 #pragma unroll
             for (int lq = 0; lq < 4; lq++) {
@@ -526,14 +532,20 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
                 // any use, so the shared-memory latency overlaps the arithmetic
                 int qcs[2];
                 RingT rts[2];
-                int2 rows[2][2];
+                int rows[2][2];
 #pragma unroll
                 for (int mq = 0; mq < 2; mq++) {
                     const int q = ir + (mq ^ b2) - m_lo;
                     qcs[mq] = (unsigned)q < (unsigned)nr ? q : nr;
-                    rts[mq] = RT[qcs[mq]];
-                    rows[mq][0] = rowA[qcs[mq]];
-                    rows[mq][1] = rowB[qcs[mq]];
+                    {  // one 16-byte load: (qt lo, qt hi, mt, W)
+                        const int4 raw = reinterpret_cast<const int4*>(RT)[qcs[mq]];
+                        rts[mq].qt = __hiloint2double(raw.y, raw.x);
+                        rts[mq].mt = raw.z;
+                        rts[mq].W = raw.w;
+                    }
+                    const int2 it = itk[qcs[mq]];
+                    rows[mq][0] = b3 ? it.y : it.x;
+                    rows[mq][1] = b3 ? it.x : it.y;
                 }
 #pragma unroll
                 for (int mq = 0; mq < 2; mq++) {
@@ -542,7 +554,7 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
                     double sl = __dmul_rn(__fma_rn(-zeta, rt.qt, tl2), kInvTwoPi);
                     int jw;
                     sl = __dsub_rn(sl, floor_fx(sl, &jw));
-                    sl = __dmul_rn(sl, rt.mtd);
+                    sl = __dmul_rn(sl, i2d_fx(rt.mt));
                     int j;
                     floor_fx(sl, &j);
                     j = (int)min((unsigned)j, (unsigned)(rt.mt - 1));
@@ -558,11 +570,12 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
                     const int ja = b4 ? j1 : j, jb = b4 ? j : j1;
 #pragma unroll
                     for (int kq = 0; kq < 2; kq++) {
-                        const int2 row = rows[mq][kq];
-                        const unsigned da = wrap_diff(ja, row.x, rt.mt), db = wrap_diff(jb, row.x, rt.mt);
+                        const int row = rows[mq][kq];
+                        const int rx = row_x(row), ry = row_y(row);
+                        const unsigned da = wrap_diff(ja, rx, rt.mt), db = wrap_diff(jb, rx, rt.mt);
                         bad = max(bad, (int)max(da, db) - rt.W);
-                        const int oa = row.y + 4 * (int)min(da, (unsigned)rt.W);
-                        const int ob = row.y + 4 * (int)min(db, (unsigned)rt.W);
+                        const int oa = ry + 4 * (int)min(da, (unsigned)rt.W);
+                        const int ob = ry + 4 * (int)min(db, (unsigned)rt.W);
                         const double wzk = kq ? wzB : wzA;
                         const double ta = fx_magic(wzk, aa), tb = fx_magic(wzk, ab);
                         unsigned char* base = reinterpret_cast<unsigned char*>(slo);
@@ -580,10 +593,27 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
                             }
                         }
 #endif
+#ifdef GTCP_DEP_CARRY
+                        // one 32-bit word takes the whole contribution v (|v| < 2^31, the
+                        // low word of the magic sum); a signed wrap of that word, seen in
+                        // the returned old value, moves +-2^32 into the high word.  The
+                        // node value hi * 2^32 + lo is the exact sum in any order.
+                        {
+                            const int va = __double2loint(ta), vb = __double2loint(tb);
+                            const int pa = atomicAdd(reinterpret_cast<int*>(base + oa), va);
+                            const int pb = atomicAdd(reinterpret_cast<int*>(base + ob), vb);
+                            const int na = pa + va, nb = pb + vb;
+                            if (((pa ^ na) & (va ^ na)) < 0)
+                                atomicAdd(reinterpret_cast<int*>(base + oa + 4 * kDepStride), va < 0 ? -1 : 1);
+                            if (((pb ^ nb) & (vb ^ nb)) < 0)
+                                atomicAdd(reinterpret_cast<int*>(base + ob + 4 * kDepStride), vb < 0 ? -1 : 1);
+                        }
+#else
                         atomicAdd(reinterpret_cast<unsigned*>(base + oa), fx_lo(ta));
                         atomicAdd(reinterpret_cast<int*>(base + oa + 4 * kDepStride), fx_hi(ta));
                         atomicAdd(reinterpret_cast<unsigned*>(base + ob), fx_lo(tb));
                         atomicAdd(reinterpret_cast<int*>(base + ob + 4 * kDepStride), fx_hi(tb));
+#endif
                     }
                 }
             }
@@ -620,13 +650,14 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
                         const int j1 = (j + 1 == mt) ? 0 : j + 1;
 #pragma unroll 1
                         for (int kq = 0; kq < 2; kq++) {
-                            const int2 row = (kq ? rowB : rowA)[qc];
+                            const int2 it = itk[qc];
+                            const int rx = row_x((kq ^ b3) ? it.y : it.x);
                             const double wzk = kq ? wzB : wzA;
 #pragma unroll 1
                             for (int u = 0; u < 2; u++) {
                                 const int ju = u ? j1 : j;
                                 // same test as the fast path: in the band and inside the window
-                                const bool in = qc < nr && wrap_diff(ju, row.x, rt.mt) < (unsigned)rt.W;
+                                const bool in = qc < nr && wrap_diff(ju, rx, rt.mt) < (unsigned)rt.W;
                                 if (in) continue;
                                 const long long v = fx_val(fx_magic(wzk, u ? a1 : a0));
                                 if (v) { red_i64(fx + fx_node(g, kq ? kp1 : kp0, m, ju, mt), v); fb++; }
@@ -647,11 +678,16 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
             for (int e = threadIdx.x; e < T.total; e += blockDim.x) {
                 const int q = colq[x];
                 if (q != 0xFF) {
+#ifdef GTCP_DEP_CARRY
+                    long long v = (long long)shi[e] * (1LL << 32) + (long long)(int)slo[e];
+#else
                     long long v = (long long)shi[e] * (1LL << kLimbBits) + (long long)slo[e];
+#endif
                     if (v != 0) {
                         DCHECK(x >= 0 && x < S && kk >= 0 && kk < P1 && q < nr);
                         const int mt = T.mt[q];
-                        int j = rowt[kk * kRowStride + q].x + (x - T.WO[q].y);
+                        int j = row_x(kk < g.P ? itab[kk * kITStride + q].x : itab[(g.P - 1) * kITStride + q].y) +
+                                (x - T.WO[q].y);
                         if (j >= mt) j -= mt;
                         red_i64(fx + fx_node(g, kk, m_lo + q, j, mt), v);
                     }
@@ -690,7 +726,7 @@ int deposit_tiled_ctas_per_sm(size_t smem_bytes, int nb) {
 
 size_t deposit_tiled_smem(int P, int nb) {
     const int cap = deposit_cap_nodes(nb);
-    return (size_t)(2 * (cap + 1)) * 4 + (size_t)(P + 1) * kRowStride * 8 + (size_t)(cap / (P + 1) + 64);
+    return (size_t)(2 * (cap + 1)) * 4 + (size_t)P * kITStride * 8 + (size_t)(cap / (P + 1) + 64);
 }
 
 void launch_deposit_tiled(const Geo& g, const PSet& s, long long n, const Tile* tiles, int max_tiles,

@@ -162,3 +162,87 @@ def test_fp32_gather_field_with_fp64_state(G, orc, Tcfg):
     orc.push(p, 2, Xa, Xb, parts["mu"], gp)
     got = ctx.get_particles()
     assert_particles_close({**{k: got[k] for k in orc.ATTRS}, "id": got["id"]}, {**Xa, "id": parts["id"]})
+
+
+# ------------------------------------------------------------------ ABI regressions (round-1 advisor findings)
+def test_step_host_twice_matches_oracle(G, orc, Tcfg):
+    """gtcp_step_host: upload, one step, download the owned state AND mu (a
+    bin inside the step reorders them together), twice in a row; each call's
+    result matches the oracle step of the previous call's output."""
+    cfg, p, g = Tcfg
+    parts = synth.load_particles(cfg, 12100, seed=7, w_amp=0.05)
+    ctx = G.Context(G.gtcp_default_params("T", bin_every=1))
+    ctx.set_particles(parts)
+    nm = orc.marker_norm(p, parts)
+    ctx.set_grid(G.GRID_MARKER, nm)
+    keys = ("psi", "theta", "zeta", "rho", "w", "mu")
+    host = [np.ascontiguousarray(parts[k]).copy() for k in keys]
+    for call in range(2):
+        state = {k: host[i].copy() for i, k in enumerate(keys)}
+        orc.step_global(p, state, nm)
+        n = ctx.step_host(host, 1)
+        assert n == 12100
+        # compare as multisets keyed by mu (mu is never written, unique per marker)
+        o1, o2 = np.argsort(host[5]), np.argsort(state["mu"])
+        assert np.array_equal(host[5][o1], state["mu"][o2])
+        for i, k in enumerate(keys[:5]):
+            if k in ("theta", "zeta"):
+                d = (host[i][o1] - state[k][o2] + math.pi) % TWO_PI - math.pi
+                assert np.max(np.abs(d)) / TWO_PI <= TOL, (call, k)
+            else:
+                assert rel_err(host[i][o1], state[k][o2]) <= TOL, (call, k)
+    ctx.close()
+
+
+def test_step_host_capacity_error(G, Tcfg):
+    cfg, p, g = Tcfg
+    parts = synth.load_particles(cfg, 1000, seed=8)
+    ctx = G.Context(G.gtcp_default_params("T"))
+    ctx.set_particles(parts)
+    ctx.set_grid(G.GRID_MARKER, np.ones(p.mpsi + 1))
+    host = [np.ascontiguousarray(parts[k]).copy() for k in ("psi", "theta", "zeta", "rho", "w", "mu")]
+    import ctypes as C
+    ptrs = (C.POINTER(C.c_double) * 6)(*[h.ctypes.data_as(C.POINTER(C.c_double)) for h in host])
+    nout = C.c_int64()
+    s = G.lib().gtcp_step_host(ctx._h, 1000, 999, ptrs, 1, C.byref(nout))  # cap < owned count
+    assert s == 6 and nout.value == 1000  # GTCP_ECAPACITY, count reported
+    ctx.close()
+
+
+def test_sample_particles_ids_fp32(G, Tcfg):
+    """precision 32 + track_ids: sampled ids are the 64-bit ids (not the fp32
+    state's element size)."""
+    cfg, p, g = Tcfg
+    parts = synth.load_particles(cfg, 5000, seed=9)
+    parts["id"] = (np.arange(5000, dtype=np.uint64) * np.uint64(2654435761) + np.uint64(1 << 40))
+    ctx = G.Context(G.gtcp_default_params("T", precision=32, track_ids=1))
+    ctx.set_particles(parts)
+    full = ctx.get_particles(("psi",))
+    idx = np.array([0, 17, 4999, 2500, 123])
+    smp = ctx.sample_particles(idx, ("psi",))
+    assert np.array_equal(smp["id"], full["id"][idx])
+    assert set(full["id"].tolist()) == set(parts["id"].tolist())
+    ctx.close()
+
+
+def test_step_reports_nonfinite(G, Tcfg):
+    """A non-finite weight makes gtcp_step return GTCP_ENONFINITE
+    instead of stepping a corrupt state silently; the deposit skips it."""
+    cfg, p, g = Tcfg
+    parts = synth.load_particles(cfg, 2000, seed=10)
+    ok = synth.load_particles(cfg, 2000, seed=10)
+    parts["w"] = parts["w"].copy()
+    parts["w"][5] = np.nan
+    ctx = G.Context(G.gtcp_default_params("T"))
+    ctx.set_particles(parts)
+    ctx.charge()
+    rho = ctx.get_grid(G.GRID_CHARGE)
+    assert np.all(np.isfinite(rho))
+    ok_sub = {k: np.delete(v, 5) for k, v in ok.items()}
+    assert rel_err(rho, orc_charge := __import__("oracle").charge_global(
+        __import__("oracle").make_params(cfg), ok_sub)) <= 1e-8
+    ctx.set_grid(G.GRID_MARKER, np.ones(p.mpsi + 1))
+    with pytest.raises(G.GtcpError) as e:
+        ctx.step(1)
+    assert e.value.status == 7  # GTCP_ENONFINITE
+    ctx.close()
