@@ -132,6 +132,21 @@ typedef struct {
     int32_t fx_shift;       /* fixed-point scale F of the last charge (2^-F units) */
 } gtcp_stats_t;
 
+/* Physics diagnostics of the current state (SPEC S:578-586 history record;
+ * paper fig:convergence P:718-729 plots chi in gyro-Bohm units).  Host copy,
+ * filled by gtcp_diag. */
+typedef struct {
+    double field_energy;    /* sum of phi^2 over the canonical nodes of all planes (phi of the
+                             * last poisson_smooth)                                            */
+    double heat_flux;       /* Q = sum_p w_p (v_par^2/2 + mu B) v_E,r(p): delta-f ion heat flux with
+                             * the gather field of the last gtcp_field (U-2, U-3), all ranks       */
+    double chi_gb;          /* chi_i / chi_GB = (Q / N) / |dT/dr|(0.5a) * omega0^2: the flux per
+                             * marker over the temperature gradient R0/L_T / R0, in units of
+                             * rho_i^2 c_s / a (qualitative; absolute values out of scope)        */
+    double sum_w;           /* sum of weights over all ranks                                    */
+    int64_t n_global;       /* markers over all ranks                                           */
+} gtcp_diag_t;
+
 /* Phase timers (CUDA events on the context stream), cumulative milliseconds
  * since the last gtcp_timings_reset. */
 enum gtcp_phase {
@@ -242,6 +257,10 @@ gtcp_status gtcp_get_grid(gtcp_ctx ctx, int which, int64_t cap, double* host);
 gtcp_status gtcp_set_grid(gtcp_ctx ctx, int which, int64_t n, const double* host);
 
 gtcp_status gtcp_stats(gtcp_ctx ctx, gtcp_stats_t* out);
+/* Diagnostics of the current live state against the current gather field
+ * (call after gtcp_field, before the push, for the fields of this stage);
+ * collective over all ranks; synchronises.  EINVAL if out is NULL. */
+gtcp_status gtcp_diag(gtcp_ctx ctx, gtcp_diag_t* out);
 gtcp_status gtcp_timings(gtcp_ctx ctx, gtcp_timings_t* out);
 gtcp_status gtcp_timings_reset(gtcp_ctx ctx);
 /* Enable (1) / disable (0) per-phase CUDA-event timing (default off). */

@@ -86,6 +86,7 @@ def lib():
                                      C.c_int32, C.c_int32, d]),
             "orc_shift_dest": (None, [P, C.c_int64, d, C.c_int32, i32]),
             "orc_bin_key": (None, [P, C.c_int64, d, d, d, d, C.c_int32, C.c_int32, C.c_int32, i64]),
+            "orc_heat_flux": (C.c_double, [P, C.c_int64, d, d, d, d, d, d, C.c_int32, C.c_int32, d]),
             "orc_omp_threads": (C.c_int, []),
             "orc_deposit_replicas": (C.c_int64, [P, C.c_int64, d, d, d, d, d, C.c_int32, C.c_int32, d, C.c_int64]),
             "orc_push_omp": (C.c_int64, [P, C.c_int32, C.c_int64, C.POINTER(d), C.POINTER(d), d,
@@ -247,6 +248,24 @@ def shift_dest(p: Params, zeta: np.ndarray, P: int) -> np.ndarray:
     out = np.zeros(len(z), np.int32)
     lib().orc_shift_dest(C.byref(p), len(z), _d(z), P, out.ctypes.data_as(C.POINTER(C.c_int32)))
     return out
+
+
+def heat_flux(p: Params, parts: dict, gradphi: np.ndarray, k0: int = 0, P: int | None = None) -> float:
+    """Diagnostic heat flux sum_p w E_kin v_E,r with the gathered field."""
+    P = p.mzetamax if P is None else P
+    a = [_f64(parts[k]) for k in ("psi", "theta", "zeta", "rho", "w", "mu")]
+    return float(lib().orc_heat_flux(C.byref(p), len(a[0]), *[_d(x) for x in a], k0, P,
+                                     _d(_f64(gradphi).ravel())))
+
+
+def field_energy(p: Params, phi: np.ndarray) -> float:
+    """Sum of phi^2 over the canonical nodes (j < mtheta) of planes 0..mzetamax-1."""
+    g = geometry(p)
+    phi = _f64(phi).reshape(-1, g.mgrid)
+    s = 0.0
+    for i in range(p.mpsi + 1):
+        s += float(np.sum(phi[:p.mzetamax, g.igrid[i]:g.igrid[i] + g.mtheta[i]] ** 2))
+    return s
 
 
 def omp_threads() -> int:

@@ -720,6 +720,33 @@ int64_t orc_push(const orc_params* p, int32_t stage, int64_t n, double* const* X
     return nrefl;
 }
 
+/* Diagnostic (fig:convergence P:718-729): delta-f ion heat
+ * flux Q = sum_p w_p E_kin,p v_E,r(p), E_kin = v_par^2/2 + mu B and
+ * v_E,r = -gbar_theta / (r omega0 B) with the gyro-averaged gradient of the
+ * local field (U-2, U-3; v_E,r = 0 with the drift-off flag).  Pinned: phi = 0
+ * or w = 0 gives 0; a field with constant g_theta gives the closed form
+ * sum w E_kin (-g_theta / (r omega0 B)) (tests/test_oracle_push.py). */
+double orc_heat_flux(const orc_params* p, int64_t n, const double* psi, const double* theta,
+                     const double* zeta, const double* rho_par, const double* w, const double* mu,
+                     int32_t k0, int32_t P, const double* gradphi) {
+    orc_geom g;
+    geom_build(p, &g);
+    orc_stencil st;
+    double q = 0.0;
+    for (int64_t ip = 0; ip < n; ip++) {
+        orc_build_stencil(p, &g, psi[ip], theta[ip], zeta[ip], mu[ip], k0, P, &st);
+        double gt = 0.0;
+        for (int c = 0; c < st.n; c++) gt += st.wgt[c] * gradphi[st.node[c] * 3 + 1];
+        double r = sqrt(2.0 * psi[ip]);
+        double B = orc_B(p, r, theta[ip]);
+        double vpar = p->omega0 * B * rho_par[ip];
+        double vEr = p->drifts ? -gt / (r * p->omega0 * B) : 0.0;
+        q += w[ip] * (0.5 * vpar * vpar + mu[ip] * B) * vEr;
+    }
+    geom_free(&g);
+    return q;
+}
+
 /* ------------------------------------------------------------------ */
 /* Shift and bin (H-1, H-4)                          */
 /* ------------------------------------------------------------------ */

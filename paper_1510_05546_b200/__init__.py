@@ -59,6 +59,11 @@ class Stats(C.Structure):
                 ("plane_clamps", C.c_int64), ("charge_global_fallback", C.c_int64), ("fx_shift", C.c_int32)]
 
 
+class Diag(C.Structure):
+    _fields_ = [("field_energy", C.c_double), ("heat_flux", C.c_double), ("chi_gb", C.c_double),
+                ("sum_w", C.c_double), ("n_global", C.c_int64)]
+
+
 class Timings(C.Structure):
     _fields_ = [("ms", C.c_double * 7), ("calls", C.c_int64 * 7), ("launches", C.c_int64),
                 ("comm_bytes", C.c_int64 * 7)]
@@ -70,7 +75,7 @@ SYMBOLS = ("gtcp_default_params", "gtcp_geometry", "gtcp_nccl_unique_id", "gtcp_
            "gtcp_poisson_smooth", "gtcp_field", "gtcp_push", "gtcp_shift", "gtcp_bin", "gtcp_step",
            "gtcp_step_host", "gtcp_get_grid", "gtcp_set_grid", "gtcp_stats", "gtcp_timings", "gtcp_timings_reset",
            "gtcp_set_timing", "gtcp_set_charge_mode", "gtcp_sample_particles", "gtcp_loopback_create",
-           "gtcp_loopback_destroy", "gtcp_init_loopback")
+           "gtcp_loopback_destroy", "gtcp_init_loopback", "gtcp_diag")
 
 _lib = None
 
@@ -111,6 +116,7 @@ def lib():
             "gtcp_get_grid": (st, [vp, C.c_int, C.c_int64, C.POINTER(C.c_double)]),
             "gtcp_set_grid": (st, [vp, C.c_int, C.c_int64, C.POINTER(C.c_double)]),
             "gtcp_stats": (st, [vp, C.POINTER(Stats)]),
+            "gtcp_diag": (st, [vp, C.POINTER(Diag)]),
             "gtcp_timings": (st, [vp, C.POINTER(Timings)]),
             "gtcp_timings_reset": (st, [vp]),
             "gtcp_set_timing": (st, [vp, C.c_int]),
@@ -303,6 +309,11 @@ class Context:
         s = Stats()
         self._chk(lib().gtcp_stats(self._h, C.byref(s)), "stats")
         return {k: getattr(s, k) for k, _ in Stats._fields_}
+
+    def diag(self) -> dict:
+        d = Diag()
+        self._chk(lib().gtcp_diag(self._h, C.byref(d)), "diag")
+        return {k: getattr(d, k) for k, _ in Diag._fields_}
 
     def set_timing(self, on: bool = True):
         self._chk(lib().gtcp_set_timing(self._h, int(on)), "set_timing")

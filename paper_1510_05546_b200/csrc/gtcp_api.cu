@@ -454,9 +454,9 @@ static gtcp_status init_ctx(const gtcp_params* p, int rank, int nranks, const vo
     CU(cudaMallocHost((void**)&c->h_dc, sizeof(DevCounters)));
     CU(cudaMallocHost((void**)&c->h_nonfinite, sizeof(int)));
     c->h_nonfinite[0] = 0;
-    CU(dalloc(&c->d_scalar, 16));
+    CU(dalloc(&c->d_scalar, 32));
     CU(dalloc(&c->d_partial, 1024));
-    CU(cudaMallocHost((void**)&c->h_scalar, 16 * sizeof(double)));
+    CU(cudaMallocHost((void**)&c->h_scalar, 32 * sizeof(double)));
     {
         std::vector<double> ones(M + 1, 1.0);
         CU(cudaMemcpy(c->nm, ones.data(), sizeof(double) * (M + 1), cudaMemcpyHostToDevice));
@@ -1286,6 +1286,41 @@ extern "C" gtcp_status gtcp_stats(gtcp_ctx c, gtcp_stats_t* out) {
     out->charge_global_fallback = c->h_dc->fallback;
     out->fx_shift = c->h_dc->fx_shift;
     if (c->h_dc->nonfinite) return set_err(c, GTCP_ENONFINITE, "non-finite particle state");
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_diag(gtcp_ctx c, gtcp_diag_t* out) {
+    CHECK_CTX(c);
+    if (!out) return GTCP_EINVAL;
+    // [0] heat flux, [1] field energy, [2] sum w, [3] n (as double); [4..7] reduced
+    PSet s = live_set(c);
+    launch_heat_flux(c->geo, s, c->n, c->gfield, c->d_scalar + 8, c->d_partial, c->st);
+    launch_field_energy(c->geo, c->phiH + c->mgrid, c->d_scalar + 9, c->d_partial, c->st);
+    launch_sum_f64(c->live[4], c->n, c->d_scalar + 10, c->d_partial, c->st);
+    const double nl = (double)c->n;
+    CU(cudaMemcpyAsync(c->d_scalar + 11, &nl, 8, cudaMemcpyHostToDevice, c->st));
+    if (c->nranks > 1) {
+        // particles are partitioned over all ranks; the grid over the toroidal
+        // ring only (replicas and radial windows hold copies of it)
+        NC(comm_allreduce(c->world, c->d_scalar + 8, c->d_scalar + 12, 1, ncclDouble, ncclSum, c->st, nullptr));
+        NC(comm_allreduce(c->tor, c->d_scalar + 9, c->d_scalar + 13, 1, ncclDouble, ncclSum, c->st, nullptr));
+        NC(comm_allreduce(c->world, c->d_scalar + 10, c->d_scalar + 14, 2, ncclDouble, ncclSum, c->st, nullptr));
+    } else {
+        CU(cudaMemcpyAsync(c->d_scalar + 12, c->d_scalar + 8, 4 * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    }
+    CU(cudaMemcpyAsync(c->h_scalar + 8, c->d_scalar + 12, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    KCHECK();
+    CU(cudaStreamSynchronize(c->st));
+    const gtcp_params& p = c->prm;
+    out->heat_flux = c->h_scalar[8];
+    out->field_energy = c->h_scalar[9];
+    out->sum_w = c->h_scalar[10];
+    out->n_global = (int64_t)c->h_scalar[11];
+    // chi_i = <Q> / |dT/dr|(0.5 a), <Q> the mean flux per marker (markers
+    // sample n0), |dT/dr| = (R0/L_T)/R0 at r = 0.5 a (prof = 1, T0 = 1);
+    // gyro-Bohm unit chi_GB = rho_i^2 c_s / a = 1 / omega0^2 (tau = 1)
+    const double grad_t = p.rlt / p.R0;
+    out->chi_gb = out->n_global > 0 ? out->heat_flux / (double)out->n_global / grad_t * p.omega0 * p.omega0 : 0.0;
     return GTCP_OK;
 }
 

@@ -147,6 +147,11 @@ void launch_marker_from_rho(const Geo& g, const double* rho, double* ringsum, cu
 void launch_ring_mean(const Geo& g, const double* ringsum, double* nm, cudaStream_t st);
 void launch_sum_f64(const double* x, long long n, double* out, double* partial, cudaStream_t st);
 void launch_sum_i64_pair(const long long* in2, long long* out, cudaStream_t st);
+// diagnostics: heat flux sum_p w E_kin v_E,r with the current gather field;
+// field energy sum phi^2 over the owned planes' canonical nodes (phi: plane 0)
+void launch_heat_flux(const Geo& g, const PSet& s, long long n, const double* gf, double* out, double* partial,
+                      cudaStream_t st);
+void launch_field_energy(const Geo& g, const double* phi, double* out, double* partial, cudaStream_t st);
 // shift (gtcp_shift.cu)
 int shift_chunks(long long n);
 void launch_shift_classify(const Geo& g, const double* zeta, const double* psi, int mode, long long n,

@@ -1455,6 +1455,91 @@ void launch_sum_f64(const double* x, long long n, double* out, double* partial, 
     g_launches += 2;
 }
 
+// ---------------------------------------------------------------------------
+// diagnostics (SPEC S:578-586 history record): the delta-f ion heat flux
+// Q = sum_p w_p E_kin,p v_E,r(p) (E_kin = v_par^2/2 + mu B, v_E,r =
+// -gbar_theta / (r Omega0 B), gbar the 4-point gyro-averaged gradient of the
+// current field, U-2/U-3) and the field energy sum phi^2 over canonical nodes.
+// Fixed grid of per-block partials, summed in block order (deterministic).
+// ---------------------------------------------------------------------------
+template <class R, class FT>
+__global__ void k_heat_flux(Geo g, PSet s, long long n, const double* __restrict__ gf, double* __restrict__ partial) {
+    double acc = 0.0;
+    const FT* gff = reinterpret_cast<const FT*>(gf);
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x) {
+        const double psi = ldp<R>(s.x[0], p), theta = ldp<R>(s.x[1], p), zeta = ldp<R>(s.x[2], p),
+                     rho_par = ldp<R>(s.x[3], p), w = ldp<R>(s.x[4], p), mu = ldp<R>(s.mu, p);
+        if (!isfinite((psi + theta + zeta + rho_par + mu) * 0.0 + w)) continue;
+        double r, invB, rho, inv_r;
+        gyro_radius(g, psi, cos_theta(theta), mu, &r, &invB, &rho, &inv_r);
+        double wz1;
+        int k = plane_of(g, zeta, &wz1) - g.k0;
+        k = min(max(k, 0), g.P - 1);
+        const double wz0 = 1.0 - wz1;
+        double gt = 0.0;
+        const FT* gk = gff + (long long)k * g.mgrid * 6;
+        gyro_stencil(g, r, theta, zeta, rho, inv_r, [&](int m, int j, int mt, double a0, double a1) {
+            const FT* rj = gk + ((long long)__ldg(g.igrid + m) + j) * 6;  // nodes j, j + 1 (duplicate at mt)
+            gt += a0 * (wz0 * (double)rj[1] + wz1 * (double)rj[4]) + a1 * (wz0 * (double)rj[7] + wz1 * (double)rj[10]);
+            (void)mt;
+        });
+        const double B = 1.0 / invB;
+        const double vpar = g.omega0 * B * rho_par;
+        const double vEr = g.drifts ? -gt * inv_r * g.inv_omega0 * invB : 0.0;
+        acc += w * (0.5 * vpar * vpar + mu * B) * vEr;
+    }
+    __shared__ double sm[32];
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int wq = 0; wq < (int)(blockDim.x >> 5); wq++) t += sm[wq];
+        partial[blockIdx.x] = t;
+    }
+}
+
+// sum of phi^2 over the canonical nodes (j < mtheta) of the owned planes 0..P-1
+__global__ void k_field_energy(Geo g, const double* __restrict__ phi, double* __restrict__ partial) {
+    double acc = 0.0;
+    const long long total = (long long)g.P * g.mgrid;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int node = (int)(e % g.mgrid);
+        const int i = __ldg(g.node_ring + node);
+        if (node - __ldg(g.igrid + i) == __ldg(g.mtheta + i)) continue;  // duplicate node
+        const double v = phi[e];
+        acc += v * v;
+    }
+    __shared__ double sm[32];
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int wq = 0; wq < (int)(blockDim.x >> 5); wq++) t += sm[wq];
+        partial[blockIdx.x] = t;
+    }
+}
+
+void launch_heat_flux(const Geo& g, const PSet& s, long long n, const double* gf, double* out, double* partial,
+                      cudaStream_t st) {
+    const int nb = 592;
+    if (g.prec32) k_heat_flux<float, float><<<nb, 256, 0, st>>>(g, s, n, gf, partial);
+    else if (g.f32field) k_heat_flux<double, float><<<nb, 256, 0, st>>>(g, s, n, gf, partial);
+    else k_heat_flux<double, double><<<nb, 256, 0, st>>>(g, s, n, gf, partial);
+    k_sum_final<<<1, 32, 0, st>>>(partial, nb, out);
+    g_launches += 2;
+}
+
+void launch_field_energy(const Geo& g, const double* phi, double* out, double* partial, cudaStream_t st) {
+    const int nb = 592;
+    k_field_energy<<<nb, 256, 0, st>>>(g, phi, partial);
+    k_sum_final<<<1, 32, 0, st>>>(partial, nb, out);
+    g_launches += 2;
+}
+
 __global__ void k_sum_i64_pair(const long long* in2, long long* out) { out[0] = in2[0] + in2[1]; }
 
 void launch_sum_i64_pair(const long long* in2, long long* out, cudaStream_t st) {

@@ -177,3 +177,28 @@ def test_step_global_finite_and_conservative(orc):
     assert np.all((parts["zeta"] >= 0) & (parts["zeta"] < 2 * math.pi))
     ch, phi, gp = out[0]
     assert np.all(np.isfinite(phi)) and np.abs(phi).max() > 0
+
+
+def test_heat_flux_closed_forms(orc):
+    """Diagnostic heat flux (SPEC S:578-586): zero field or zero weights give 0;
+    a field whose theta component is the constant c everywhere (gather exact,
+    U-2) gives the closed form sum w (v_par^2/2 + mu B) (-c / (r omega0 B))."""
+    cfg = synth.config("T")
+    p = orc.make_params(cfg)
+    g = orc.geometry(p)
+    parts = synth.load_particles(cfg, 3000, seed=12, w_amp=0.1)
+    zero = np.zeros((p.mzetamax + 1, g.mgrid, 3))
+    assert orc.heat_flux(p, parts, zero) == 0.0
+    c = 0.37
+    gp = zero.copy()
+    gp[..., 1] = c
+    gp[..., 0] = 0.2  # g_r and g_par do not enter v_E,r
+    gp[..., 2] = -1.3
+    r = np.sqrt(2 * parts["psi"])
+    B = 1.0 / (1.0 + r / p.R0 * np.cos(parts["theta"]))
+    vpar = p.omega0 * B * parts["rho"]
+    want = np.sum(parts["w"] * (0.5 * vpar ** 2 + parts["mu"] * B) * (-c / (r * p.omega0 * B)))
+    got = orc.heat_flux(p, parts, gp)
+    assert abs(got - want) <= 1e-12 * np.sum(np.abs(parts["w"] * (0.5 * vpar ** 2 + parts["mu"] * B) * c / (r * p.omega0 * B)))
+    w0 = dict(parts, w=np.zeros_like(parts["w"]))
+    assert orc.heat_flux(p, w0, gp) == 0.0

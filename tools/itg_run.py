@@ -1,10 +1,14 @@
-"""ITG demonstration: a nonlinear delta-f run on a class-A
-grid, printing the field energy sum(phi^2) and max|w| every `--every` steps.
-Linear ITG growth shows as a straight line in log(energy) until saturation.
+"""ITG workload (SPEC acceptance 11 as a qualitative stand-in
+for fig:convergence P:718-729): a nonlinear delta-f Cyclone run on a class-A
+grid, writing the history record of SPEC S:91 / S:578-586 every `--every`
+steps: step, time, field_energy, chi_gb, total_weight, particle_count
+(gtcp_diag).  Linear ITG growth shows as a straight line in log(field energy)
+until saturation; `--check` fits it.
 
-  python tools/itg_run.py --steps 400 --every 20 --micell 20
+  python tools/itg_run.py --steps 600 --every 10 --micell 20 --out profiles/r02_itg_history.csv --check
 """
 import argparse
+import csv
 import json
 import math
 import os
@@ -12,30 +16,76 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
-import torch  # noqa: E402
 
 import paper_1510_05546_b200 as G  # noqa: E402
 
-ap = argparse.ArgumentParser()
-ap.add_argument("--size", default="A")
-ap.add_argument("--steps", type=int, default=400)
-ap.add_argument("--every", type=int, default=20)
-ap.add_argument("--micell", type=int, default=20)
-ap.add_argument("--w-amp", type=float, default=1e-3)
-a = ap.parse_args()
-torch.cuda.set_device(0)
-p = G.gtcp_default_params(a.size, micell=a.micell, w_init_amp=a.w_amp)
-ctx = G.Context(p)
-ctx.load()
-rows = []
-for s in range(0, a.steps + 1, a.every):
-    if s:
-        ctx.step(a.every)
-    ctx.charge()  # diagnostics only: the field of the current state
-    ctx.poisson_smooth()
-    phi = ctx.get_grid(G.GRID_PHI)
-    st = ctx.stats()
-    e = float(np.sum(phi * phi))
-    rows.append({"step": s, "t": s * p.dt, "field_energy": e, "log_e": math.log(e) if e > 0 else None,
-                 "max_abs_w": st["max_abs_w"], "n": st["n_global"]})
-    print(json.dumps(rows[-1]), flush=True)
+
+def run(size="A", steps=600, every=10, micell=20, w_amp=1e-3, seed=2, out=None, echo=True):
+    import torch
+    torch.cuda.set_device(0)
+    p = G.gtcp_default_params(size, micell=micell, w_init_amp=w_amp, seed=seed)
+    ctx = G.Context(p)
+    ctx.load()
+    rows = []
+    for s in range(0, steps + 1, every):
+        if s:
+            ctx.step(every)
+        # diagnostics of the current state: its charge, potential and field
+        ctx.charge()
+        ctx.poisson_smooth()
+        ctx.field()
+        d = ctx.diag()
+        rows.append({"step": s, "time": s * p.dt, "field_energy": d["field_energy"], "chi_gb": d["chi_gb"],
+                     "total_weight": d["sum_w"], "particle_count": d["n_global"]})
+        if echo:
+            print(json.dumps(rows[-1]), flush=True)
+    ctx.close()
+    if out:
+        with open(out, "w", newline="") as f:
+            wr = csv.DictWriter(f, fieldnames=list(rows[0]))
+            wr.writeheader()
+            wr.writerows(rows)
+    return rows
+
+
+def check(rows, min_steps=200):
+    """SPEC acceptance 11: an interval of exponential field-energy growth
+    (log-linear fit R^2 >= 0.98 over >= min_steps steps) followed by
+    saturation (the growth rate over the last quarter of the run below 10 % of
+    the fitted linear-phase rate).  Returns a dict with the fit."""
+    t = np.array([r["time"] for r in rows])
+    st = np.array([r["step"] for r in rows])
+    le = np.log(np.maximum(np.array([r["field_energy"] for r in rows]), 1e-300))
+    best = None
+    for a in range(len(rows)):
+        for b in range(a + 2, len(rows)):
+            if st[b] - st[a] < min_steps:
+                continue
+            k, c = np.polyfit(t[a:b + 1], le[a:b + 1], 1)
+            res = le[a:b + 1] - (k * t[a:b + 1] + c)
+            r2 = 1 - np.sum(res ** 2) / max(np.sum((le[a:b + 1] - le[a:b + 1].mean()) ** 2), 1e-300)
+            if r2 >= 0.98 and k > 0 and (best is None or k * (t[b] - t[a]) > best["gain"]):
+                best = {"t0": float(t[a]), "t1": float(t[b]), "rate": float(k), "r2": float(r2),
+                        "gain": float(k * (t[b] - t[a])), "b": b}
+    if best is None:
+        return {"ok": False, "reason": "no exponential phase"}
+    tail = len(rows) * 3 // 4
+    late = float(np.polyfit(t[tail:], le[tail:], 1)[0]) if len(rows) - tail >= 3 else float("nan")
+    best["late_rate"] = late
+    best["ok"] = bool(t[-1] > best["t1"] and late < 0.1 * best["rate"])
+    return best
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--size", default="A")
+    ap.add_argument("--steps", type=int, default=600)
+    ap.add_argument("--every", type=int, default=10)
+    ap.add_argument("--micell", type=int, default=20)
+    ap.add_argument("--w-amp", type=float, default=1e-3)
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--check", action="store_true")
+    a = ap.parse_args()
+    rows = run(a.size, a.steps, a.every, a.micell, a.w_amp, out=a.out)
+    if a.check:
+        print(json.dumps({"check": check(rows)}), flush=True)
