@@ -154,6 +154,8 @@ def workload_config(size: str, n_gpus: int, args) -> dict:
     marker count, decomposition."""
     import synth
     over = {"micell": args.micell} if args.micell else {}
+    if args.mzetamax:
+        over["mzetamax"] = args.mzetamax
     cfg = synth.config(size, **over)
     # grid size from the product's host geometry (G-1..G-2); no oracle here
     import paper_1510_05546_b200 as G
@@ -213,6 +215,8 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     size = args.size or ("A" if world == 1 else "B")
     over = {"micell": args.micell} if args.micell else {}
+    if args.mzetamax:
+        over["mzetamax"] = args.mzetamax
     ntor = world // (args.nradial * args.npartdom)
     assert ntor * args.nradial * args.npartdom == world, "GPUs must equal ntoroidal * nradial * npartdom"
     p = G.gtcp_default_params(size, ntoroidal=ntor, nradial=args.nradial, npartdom=args.npartdom,
@@ -224,6 +228,10 @@ def run_gpu(args):
         nccl_id = obj[0]
     stream = torch.cuda.Stream()
     ctx = G.Context(p, rank, world, nccl_id, stream.cuda_stream)
+    if args.push_mode:
+        ctx.set_push_mode(args.push_mode)  # ablation: loop fission
+    if args.charge_mode:
+        ctx.set_charge_mode(args.charge_mode)  # ablation: global-atomic deposit
     ctx.load()
     info = ctx.get_info()
     n_local = info.n_local
@@ -406,7 +414,11 @@ def main():
     ap.add_argument("--nradial", type=int, default=1)
     ap.add_argument("--npartdom", type=int, default=1)
     ap.add_argument("--micell", type=int, default=None)
+    ap.add_argument("--mzetamax", type=int, default=None)
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32])
+    # ablations of the paper's own kernel designs
+    ap.add_argument("--push-mode", type=int, default=0, choices=[0, 1])
+    ap.add_argument("--charge-mode", type=int, default=0, choices=[0, 1])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

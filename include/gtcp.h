@@ -286,6 +286,11 @@ gtcp_status gtcp_init_loopback(const gtcp_params* p, int rank, int nranks, void*
 /* Test hooks: select the charge kernel (0 = smem-tiled, 1 = direct global
  * fixed-point atomics) -- both are product CUDA paths. */
 gtcp_status gtcp_set_charge_mode(gtcp_ctx ctx, int mode);
+/* Ablation hook: 0 = fused gather + push (default); 1 = the
+ * paper's Xeon Phi loop fission: a gather kernel writes the
+ * gyro-averaged gradient (3 doubles per particle) to HBM, an update kernel
+ * reads it (fp64 state only; other precisions stay fused).  Same results. */
+gtcp_status gtcp_set_push_mode(gtcp_ctx ctx, int mode);
 
 #ifdef __cplusplus
 }

@@ -95,6 +95,8 @@ struct gtcp_ctx_s {
     long long movers_sent = 0, movers_recv = 0;
     // charge config
     int charge_mode = 0;
+    int push_mode = 0;          // 1: loop-fission ablation of the push
+    double* g3 = nullptr;       // its gbar arrays (3 x cap), allocated on first use
     int dep_ctas = 0, dep_cap_nodes = 0, dep_nb = 3;
     size_t dep_smem = 0;
     // timing
@@ -573,7 +575,7 @@ extern "C" void gtcp_destroy(gtcp_ctx c) {
     F(c->d_mtheta); F(c->d_igrid); F(c->d_itran); F(c->d_qtinv); F(c->d_node_ring); F(c->d_pois);
     for (int d = 0; d < 12; d++) { F(c->sendL[d]); F(c->sendR[d]); F(c->recvL[d]); F(c->recvR[d]); }
     F(c->sidL); F(c->sidR); F(c->ridL); F(c->ridR); F(c->cls); F(c->bcount); F(c->holes); F(c->fills); F(c->midx); F(c->d_nkeep);
-    F(c->d_counts);
+    F(c->d_counts); F(c->g3);
     if (c->h_counts) cudaFreeHost(c->h_counts);
     if (c->h_dc) cudaFreeHost(c->h_dc);
     if (c->h_nonfinite) cudaFreeHost(c->h_nonfinite);
@@ -873,7 +875,7 @@ static void push_range(gtcp_ctx c, double* const* src, double* const* base, doub
     c->cls_ready = fuse;
     if (c->n > 0)
         launch_push3(c->geo, src, base, out, c->mu, c->n, h, c->gfield, c->dc, c->st, fuse ? c->cls : nullptr,
-                     fuse ? cntL : nullptr, fuse ? cntR : nullptr);
+                     fuse ? cntL : nullptr, fuse ? cntR : nullptr, c->push_mode == 1 ? c->g3 : nullptr);
 }
 
 extern "C" gtcp_status gtcp_push(gtcp_ctx c, int stage) {
@@ -1350,6 +1352,14 @@ extern "C" gtcp_status gtcp_timings_reset(gtcp_ctx c) {
 extern "C" gtcp_status gtcp_set_timing(gtcp_ctx c, int enable) {
     CHECK_CTX(c);
     c->timing = enable != 0;
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_set_push_mode(gtcp_ctx c, int mode) {
+    CHECK_CTX(c);
+    if (mode != 0 && mode != 1) return GTCP_EINVAL;
+    if (mode == 1 && !c->g3) CU(dalloc(&c->g3, 3 * c->cap));
+    c->push_mode = mode;
     return GTCP_OK;
 }
 

@@ -103,7 +103,8 @@ void launch_fx_to_real(const Geo& g, const long long* fx, double* rho, const Dev
                        cudaStream_t st);
 void launch_push3(const Geo& g, const double* const src[5], const double* const base[5], double* const out[5],
                   const double* mu, long long n, double h, const double* gfield, DevCounters* dc, cudaStream_t st,
-                  unsigned char* cls = nullptr, unsigned* cntL = nullptr, unsigned* cntR = nullptr);
+                  unsigned char* cls = nullptr, unsigned* cntL = nullptr, unsigned* cntR = nullptr,
+                  double* g3 = nullptr);  // g3 != null: loop-fission ablation (3 n doubles of gbar)
 void launch_wmax(const double* w, long long n, DevCounters* dc, cudaStream_t st);
 void launch_bin_keys(const Geo& g, const PSet& s, long long n, unsigned* key, unsigned* rank, unsigned* count,
                      cudaStream_t st);

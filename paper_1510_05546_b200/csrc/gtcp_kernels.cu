@@ -821,12 +821,15 @@ __device__ __forceinline__ double warp_max(double v) {
 // the source state (psi, theta, zeta, rho_par, w), mu and the base state.
 // Counts reflections / plane clamps into the caller's registers.
 // FT: storage type of the gather field (double; float with the fp32 particle
-// state of precision 32), arithmetic always fp64
-template <int GU = 8, class FT = double>
+// state of precision 32), arithmetic always fp64.
+// MODE 0: fused gather + update (the product).  Loop-fission ablation of the
+// paper's Xeon Phi push: MODE 1 only gathers gbar into gio[0..2],
+// MODE 2 only updates from gio.
+template <int GU = 8, class FT = double, int MODE = 0>
 __device__ __forceinline__ void push_one(const Geo& g, const RingTab* __restrict__ rt, double psi, double theta,
                                          double zeta, double rho_par, double w, double mu, const double* base,
                                          double h, const double* __restrict__ gf, double* X, long long& refl,
-                                         long long& clamps) {
+                                         long long& clamps, double* gio = nullptr) {
     // U-1
     double st, ct;
     sincos_theta(theta, &st, &ct);
@@ -838,6 +841,12 @@ __device__ __forceinline__ void push_one(const Geo& g, const RingTab* __restrict
     const double B = q * inv_qB;
     const double inv_q = invB * inv_qB;
     // U-2 gather
+    double gr, gt, gp;
+    if constexpr (MODE == 2) {
+        gr = gio[0];
+        gt = gio[1];
+        gp = gio[2];
+    } else {
     double wz1;
     int kg = plane_of(g, zeta, &wz1);
     int k = kg - g.k0;
@@ -899,7 +908,16 @@ __device__ __forceinline__ void push_one(const Geo& g, const RingTab* __restrict
         p1 = fma(a0, v2.y, fma(a1, v5.y, p1));
     }
     const double wz0q = 0.25 * wz0, wz1q = 0.25 * wz1;
-    const double gr = wz0q * r0 + wz1q * r1, gt = wz0q * t0 + wz1q * t1, gp = wz0q * p0 + wz1q * p1;
+    gr = wz0q * r0 + wz1q * r1;
+    gt = wz0q * t0 + wz1q * t1;
+    gp = wz0q * p0 + wz1q * p1;
+    if constexpr (MODE == 1) {
+        gio[0] = gr;
+        gio[1] = gt;
+        gio[2] = gp;
+        return;
+    }
+    }
     // U-3 drifts
     const double vpar = g.omega0 * B * rho_par;
     const double iOB = g.inv_omega0 * invB;  // 1 / (omega0 B)
@@ -970,9 +988,10 @@ __device__ __forceinline__ void push_epilogue(DevCounters* dc, double wmax, long
     if (nonfinite) dc->nonfinite = 1;
 }
 
-template <int MINB, bool CS, int GU = 8, class R = double, class FT = R>
+template <int MINB, bool CS, int GU = 8, class R = double, class FT = R, int MODE = 0>
 __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long long n, double h,
-                                             const double* __restrict__ gf, DevCounters* dc) {
+                                             const double* __restrict__ gf, DevCounters* dc,
+                                             double* __restrict__ g3 = nullptr) {
     extern __shared__ RingTab rt_dyn[];
     load_ring_tab(g, rt_dyn);
     double wmax = 0.0;
@@ -985,8 +1004,23 @@ __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long lon
         double base[5], X[5];
 #pragma unroll
         for (int d = 0; d < 5; d++) base[d] = ld(pp.base[d]);
-        push_one<GU, FT>(g, rt_dyn, ld(pp.src[0]), ld(pp.src[1]), ld(pp.src[2]), ld(pp.src[3]), ld(pp.src[4]), ld(pp.mu),
-                 base, h, gf, X, refl, clamps);
+        if constexpr (MODE == 1) {  // fission, gather loop: gbar to HBM (3 arrays)
+            double gio[3];
+            push_one<GU, FT, 1>(g, rt_dyn, ld(pp.src[0]), ld(pp.src[1]), ld(pp.src[2]), 0.0, 0.0, ld(pp.mu), base, h,
+                                gf, X, refl, clamps, gio);
+            __stcs(g3 + p, gio[0]);
+            __stcs(g3 + n + p, gio[1]);
+            __stcs(g3 + 2 * n + p, gio[2]);
+            continue;
+        }
+        if constexpr (MODE == 2) {  // fission, update loop: gbar from HBM
+            double gio[3] = {__ldcs(g3 + p), __ldcs(g3 + n + p), __ldcs(g3 + 2 * n + p)};
+            push_one<GU, FT, 2>(g, rt_dyn, ld(pp.src[0]), ld(pp.src[1]), ld(pp.src[2]), ld(pp.src[3]), ld(pp.src[4]),
+                                ld(pp.mu), base, h, gf, X, refl, clamps, gio);
+        } else {
+            push_one<GU, FT>(g, rt_dyn, ld(pp.src[0]), ld(pp.src[1]), ld(pp.src[2]), ld(pp.src[3]), ld(pp.src[4]),
+                             ld(pp.mu), base, h, gf, X, refl, clamps);
+        }
         // one test: a NaN or Inf in any component survives the product with 0
         if (!isfinite((X[0] + X[1] + X[2] + X[3]) * 0.0 + X[4])) nonfinite = 1;
 #pragma unroll
@@ -1013,7 +1047,7 @@ __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long lon
 
 void launch_push3(const Geo& g, const double* const src[5], const double* const base[5], double* const out[5],
                   const double* mu, long long n, double h, const double* gfield, DevCounters* dc,
-                  cudaStream_t st, unsigned char* cls, unsigned* cntL, unsigned* cntR) {
+                  cudaStream_t st, unsigned char* cls, unsigned* cntL, unsigned* cntR, double* g3) {
     if (n <= 0) return;
     PushPtrs pp;
     for (int d = 0; d < 5; d++) {
@@ -1030,7 +1064,12 @@ void launch_push3(const Geo& g, const double* const src[5], const double* const 
     // field windows, a texture-path gather) were all slower
     int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
     size_t smr = (g.mpsi + 1) * sizeof(RingTab);
-    if (g.prec32) k_push<2, true, 8, float><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
+    if (g3 && !g.prec32 && !g.f32field) {
+        // loop-fission ablation: gather loop, then update loop
+        k_push<2, true, 8, double, double, 1><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc, g3);
+        k_push<2, true, 8, double, double, 2><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc, g3);
+        g_launches++;
+    } else if (g.prec32) k_push<2, true, 8, float><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
     else if (g.f32field) k_push<2, true, 8, double, float><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
     else k_push<2, true, 8, double><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
     g_launches++;

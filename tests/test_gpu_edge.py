@@ -246,3 +246,24 @@ def test_step_reports_nonfinite(G, Tcfg):
         ctx.step(1)
     assert e.value.status == 7  # GTCP_ENONFINITE
     ctx.close()
+
+
+def test_push_loop_fission_matches_fused(G, orc, Tcfg):
+    """Loop-fission ablation (gather loop writing gbar, then update
+    loop) computes the same stage as the fused push."""
+    cfg, p, g = Tcfg
+    parts = synth.load_particles(cfg, 12100, seed=13, w_amp=0.1)
+    gp = _smooth_field(orc, p, g)
+    outs = []
+    for mode in (0, 1):
+        ctx = ctx_for(G, "T")
+        ctx.set_push_mode(mode)
+        ctx.set_particles(parts)
+        ctx.set_grid(G.GRID_GRADPHI, gp)
+        ctx.push(1)
+        ctx.push(2)
+        outs.append(ctx.get_particles())
+        ctx.close()
+    o1, o2 = np.argsort(outs[0]["id"]), np.argsort(outs[1]["id"])
+    for k in ("psi", "theta", "zeta", "rho", "w"):
+        assert rel_err(outs[1][k][o2], outs[0][k][o1]) <= 1e-14, k
