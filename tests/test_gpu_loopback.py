@@ -5,8 +5,9 @@ charge merge, section and ring allreduces, potential halos,
 plane-split Poisson broadcasts, shift counts and payload -- with
 one cudaMemcpyAsync per message.  The library code path above the transport
 is the one NCCL runs (tests/dist_parity.py).  Layouts: toroidal 2 and 4,
-particle replicas 2, radial windows 2 (fp32 state), toroidal x radial 2 x 2,
-at T and at class-A geometry with 1 M markers; plus the fixed-point scale
+particle replicas 2, radial windows 2 (fp32 state) and 4, toroidal x radial
+2 x 2 and 2 x 4 (8 ranks), at T and at class-A geometry with 0.4-1 M markers;
+plus the fixed-point scale
 agreement regressions (replicas / toroidal ranks whose max|w| fall in
 different binades)."""
 import math
@@ -43,6 +44,8 @@ CASES = [
     dict(size="T", world=2, npartdom=2, mzetamax=8),
     dict(size="T", world=2, nradial=2, mzetamax=8),
     dict(size="T", world=4, nradial=2, mzetamax=8),
+    dict(size="T", world=4, nradial=4, mzetamax=8),               # general radial decomposition
+    dict(size="A", world=8, nradial=4, nparts=400_000, steps=1, mzetamax=8),  # 2 toroidal x 4 radial
     dict(size="A", world=2, nparts=1_000_000, steps=1),
     dict(size="A", world=4, nparts=1_000_000, steps=1),
     dict(size="A", world=2, npartdom=2, nparts=1_000_000, steps=1),

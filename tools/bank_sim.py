@@ -91,7 +91,7 @@ def build(size, mzetamax, ring_frac, tile_max, nmu, seed, layout):
     S = 0
     for q in range(nr):
         col[q] = S
-        S += W[q] + 1
+        S += W[q] + 1 + layout.get("ring_gap", 0)
         if layout.get("ring_align"):
             S += (-S) % layout["ring_align"]
     pad = layout.get("pad", 16)
