@@ -418,7 +418,7 @@ def main():
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32])
     # ablations of the paper's own kernel designs
     ap.add_argument("--push-mode", type=int, default=0, choices=[0, 1])
-    ap.add_argument("--charge-mode", type=int, default=0, choices=[0, 1])
+    ap.add_argument("--charge-mode", type=int, default=0, choices=[0, 1, 2])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -283,8 +283,12 @@ void gtcp_loopback_destroy(void* hub);
 gtcp_status gtcp_init_loopback(const gtcp_params* p, int rank, int nranks, void* hub, void* cuda_stream,
                                gtcp_ctx* out);
 
-/* Test hooks: select the charge kernel (0 = smem-tiled, 1 = direct global
- * fixed-point atomics) -- both are product CUDA paths. */
+/* Test / ablation hooks: select the charge kernel -- 0 = smem-tiled (the
+ * product), 1 = direct global fixed-point atomics (the paper's Kepler-style
+ * cooperative atomics), 2 = the paper's Fermi update binning
+ * (P:336-353): the 4 gyro-points of every particle binned by their own cell at
+ * every charge, one thread per super-cell, even/odd twin shared-memory copies.
+ * All three give the bitwise-identical fixed-point grid. */
 gtcp_status gtcp_set_charge_mode(gtcp_ctx ctx, int mode);
 /* Ablation hook: 0 = fused gather + push (default); 1 = the
  * paper's Xeon Phi loop fission: a gather kernel writes the

@@ -96,6 +96,10 @@ struct gtcp_ctx_s {
     // charge config
     int charge_mode = 0;
     int push_mode = 0;          // 1: loop-fission ablation of the push
+    // charge mode 2 (update-binning ablation): point records and segments
+    unsigned *pkey = nullptr, *prank = nullptr, *prec = nullptr;
+    int4* psegs = nullptr;
+    int npsegs = 0;
     double* g3 = nullptr;       // its gbar arrays (3 x cap), allocated on first use
     int dep_ctas = 0, dep_cap_nodes = 0, dep_nb = 3;
     size_t dep_smem = 0;
@@ -575,7 +579,7 @@ extern "C" void gtcp_destroy(gtcp_ctx c) {
     F(c->d_mtheta); F(c->d_igrid); F(c->d_itran); F(c->d_qtinv); F(c->d_node_ring); F(c->d_pois);
     for (int d = 0; d < 12; d++) { F(c->sendL[d]); F(c->sendR[d]); F(c->recvL[d]); F(c->recvR[d]); }
     F(c->sidL); F(c->sidR); F(c->ridL); F(c->ridR); F(c->cls); F(c->bcount); F(c->holes); F(c->fills); F(c->midx); F(c->d_nkeep);
-    F(c->d_counts); F(c->g3);
+    F(c->d_counts); F(c->g3); F(c->pkey); F(c->prank); F(c->prec); F(c->psegs);
     if (c->h_counts) cudaFreeHost(c->h_counts);
     if (c->h_dc) cudaFreeHost(c->h_dc);
     if (c->h_nonfinite) cudaFreeHost(c->h_nonfinite);
@@ -715,6 +719,12 @@ static gtcp_status deposit_fx(gtcp_ctx c) {
     launch_fx_scale(c->dc, c->st);
     CU(cudaMemsetAsync(c->fx, 0, (size_t)(c->P + 1) * c->mgrid * sizeof(long long), c->st));
     long long tiled_end = 0;
+    if (c->charge_mode == 2) {
+        launch_deposit_points(g, s, c->n, c->fx, c->dc, c->pkey, c->prank, c->prec, c->count, c->offset, c->scan_tmp,
+                              c->psegs, c->npsegs, c->st);
+        KCHECK();
+        return GTCP_OK;
+    }
     if (c->charge_mode == 0 && c->n_binned > 0) {
         launch_deposit_tiled(g, s, std::min(c->n, c->n_binned), c->tiles, c->max_tiles, c->fx, c->dc, c->dep_ctas,
                              c->dep_smem, c->dep_cap_nodes, c->dep_nb, c->st);
@@ -1365,7 +1375,22 @@ extern "C" gtcp_status gtcp_set_push_mode(gtcp_ctx c, int mode) {
 
 extern "C" gtcp_status gtcp_set_charge_mode(gtcp_ctx c, int mode) {
     CHECK_CTX(c);
-    if (mode != 0 && mode != 1) return GTCP_EINVAL;
+    if (mode < 0 || mode > 2) return GTCP_EINVAL;
+    if (mode == 2 && !c->pkey) {
+        // point records (4 per particle) and the (interval, ring, 256-cell) segments
+        if (4 * c->cap >= (1LL << 32)) return set_err(c, GTCP_ECAPACITY, "charge mode 2: too many points");
+        CU(dalloc(&c->pkey, 4 * c->cap));
+        CU(dalloc(&c->prank, 4 * c->cap));
+        CU(dalloc(&c->prec, 4 * c->cap));
+        std::vector<int4> sg;
+        for (int k = 0; k < c->P; k++)
+            for (int i = 0; i < c->prm.mpsi; i++)
+                for (int c0 = 0; c0 < c->mtheta[i]; c0 += 256)
+                    sg.push_back(make_int4(k, i, c0, std::min(c0 + 255, c->mtheta[i] - 1)));
+        c->npsegs = (int)sg.size();
+        CU(dalloc(&c->psegs, sg.size()));
+        CU(cudaMemcpy(c->psegs, sg.data(), sizeof(int4) * sg.size(), cudaMemcpyHostToDevice));
+    }
     c->charge_mode = mode;
     return GTCP_OK;
 }

@@ -98,6 +98,11 @@ size_t deposit_tiled_smem(int P, int nb);
 int deposit_tiled_ctas_per_sm(size_t smem_bytes, int nb);  // after configure_deposit_tiled
 void launch_deposit_direct(const Geo& g, const PSet& s, long long begin, long long n, long long* fx,
                            DevCounters* dc, cudaStream_t st);
+// charge ablation: the paper's update-binning deposit (points binned by cell
+// every charge, one thread per super-cell, twin shared-memory copies)
+void launch_deposit_points(const Geo& g, const PSet& s, long long n, long long* fx, DevCounters* dc, unsigned* pkey,
+                           unsigned* prank, unsigned* rec, unsigned* count, unsigned* offset, unsigned* scan_tmp,
+                           const int4* segs, int nseg, cudaStream_t st);
 void launch_fx_scale(DevCounters* dc, cudaStream_t st);
 void launch_fx_to_real(const Geo& g, const long long* fx, double* rho, const DevCounters* dc, int planes,
                        cudaStream_t st);

@@ -95,12 +95,23 @@ __device__ __forceinline__ int plane_of(const Geo& g, double zeta, double* wz1) 
 // (point, ring) calls fn(m, j, mt, a0, a1) with a0/a1 = 1/4 * wp * wt0/wt1,
 // the weights of label nodes j and j+1 (j+1 may equal mt: the duplicate).
 template <class Fn>
+__device__ __forceinline__ void gyro_point(const Geo& g, double r, double theta, double zeta, double rho,
+                                           double inv_r, int l, Fn&& fn);
+
+template <class Fn>
 __device__ __forceinline__ void gyro_stencil(const Geo& g, double r, double theta, double zeta, double rho,
                                              double inv_r, Fn&& fn) {
-    // explicit roundings: the same bits in every kernel that inlines this
-    const double rho_r = __dmul_rn(rho, inv_r);
 #pragma unroll
-    for (int l = 0; l < 4; l++) {
+    for (int l = 0; l < 4; l++) gyro_point(g, r, theta, zeta, rho, inv_r, l, fn);
+}
+
+// one gyro-point l of gyro_stencil (explicit roundings: the same bits in
+// every kernel that inlines this)
+template <class Fn>
+__device__ __forceinline__ void gyro_point(const Geo& g, double r, double theta, double zeta, double rho,
+                                           double inv_r, int l, Fn&& fn) {
+    const double rho_r = __dmul_rn(rho, inv_r);
+    {
         double rl = r, tl = theta;
         if (l == 0) rl = __dadd_rn(r, rho);
         if (l == 2) rl = __dsub_rn(r, rho);
@@ -700,6 +711,198 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
         __syncthreads();
     }
     if (threadIdx.x == 0 && s_fallback) atomicAdd((unsigned long long*)&dc->fallback, s_fallback);
+}
+
+// ---------------------------------------------------------------------------
+// charge ablation: the paper's Fermi/Kepler "update
+// binning" deposit.  Every charge, the 4 gyro-points of every
+// particle are binned by the cell of the point itself (super-cell = one label
+// cell c of ring i in plane interval k), which turns the gyrokinetic deposit
+// into a standard one whose footprint spans one cell: then each thread of a
+// CTA deposits all the points of one super-cell, consecutive threads take
+// adjacent super-cells, and threads of even and odd index accumulate into two
+// separate copies of the CTA's partial grid in shared memory (the paper's
+// twin copies), flushed to the global grid once.  Same contributions and
+// fixed-point arithmetic as the product kernels (bitwise-identical grid).
+// ---------------------------------------------------------------------------
+// point key = (k * mgrid + igrid_i + c) of gyro-point l of the particle
+__device__ __forceinline__ unsigned point_key(const Geo& g, double r, double theta, double zeta, double rho,
+                                              double inv_r, int l, int k) {
+    const double rho_r = __dmul_rn(rho, inv_r);
+    double rl = r, tl = theta;
+    if (l == 0) rl = __dadd_rn(r, rho);
+    if (l == 2) rl = __dsub_rn(r, rho);
+    if (l == 1) tl = __dadd_rn(theta, rho_r);
+    if (l == 3) tl = __dsub_rn(theta, rho_r);
+    rl = fmin(fmax(rl, g.a0), g.a1);
+    const double x = __dmul_rn(__dsub_rn(rl, g.a0), g.inv_dr);
+    int i;
+    floor_fx(x, &i);
+    i = min(max(i, 0), g.mpsi - 1);
+    const int mt = __ldg(g.mtheta + i);
+    double sl = __dmul_rn(__fma_rn(-zeta, __ldg(g.qtinv + i), tl), kInvTwoPi);
+    int jw;
+    sl = __dsub_rn(sl, floor_fx(sl, &jw));
+    sl = __dmul_rn(sl, (double)mt);
+    int c;
+    floor_fx(sl, &c);
+    c = (int)min((unsigned)c, (unsigned)(mt - 1));
+    return (unsigned)(k * g.mgrid + __ldg(g.igrid + i) + c);
+}
+
+template <class R>
+__global__ void k_point_keys(Geo g, PSet s, long long n, unsigned* __restrict__ pkey, unsigned* __restrict__ prank,
+                             unsigned* __restrict__ count) {
+    const int lane = threadIdx.x & 31;
+    for (long long q0 = (long long)blockIdx.x * blockDim.x; q0 < 4 * n; q0 += (long long)gridDim.x * blockDim.x) {
+        const long long q = q0 + threadIdx.x;  // point q = 4 p + l
+        const bool act = q < 4 * n;
+        unsigned key = 0xffffffffu;
+        if (act) {
+            const long long p = q >> 2;
+            const double psi = ldp<R>(s.x[0], p), theta = ldp<R>(s.x[1], p), zeta = ldp<R>(s.x[2], p),
+                         mu = ldp<R>(s.mu, p);
+            double r, invB, rho, inv_r;
+            gyro_radius(g, psi, cos_theta(theta), mu, &r, &invB, &rho, &inv_r);
+            double wz1;
+            int k = plane_of(g, zeta, &wz1) - g.k0;
+            k = min(max(k, 0), g.P - 1);
+            key = point_key(g, r, theta, zeta, rho, inv_r, (int)(q & 3), k);
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        const int leader = __ffs(peers) - 1;
+        unsigned base = 0;
+        if (act && lane == leader) base = atomicAdd(count + key, (unsigned)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (act) {
+            pkey[q] = key;
+            prank[q] = base + __popc(peers & ((1u << lane) - 1u));
+        }
+    }
+}
+
+__global__ void k_point_scatter(const unsigned* __restrict__ pkey, const unsigned* __restrict__ prank,
+                                const unsigned* __restrict__ offset, long long npts, unsigned* __restrict__ rec) {
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < npts; q += (long long)gridDim.x * blockDim.x)
+        rec[offset[pkey[q]] + prank[q]] = (unsigned)q;
+}
+
+// One CTA per segment of up to blockDim super-cells of one (interval, ring):
+// window = planes k, k+1 x rings i, i+1 x label ranges, twin copies.
+static constexpr int kPtWin = 1280;  // window nodes per copy (2 planes x 2 rings x labels)
+template <class R>
+__global__ void __launch_bounds__(256) k_deposit_points(Geo g, PSet s, const unsigned* __restrict__ offset,
+                                                      const unsigned* __restrict__ rec, const int4* __restrict__ segs,
+                                                      long long* __restrict__ fx, DevCounters* dc) {
+    __shared__ unsigned slo[2][kPtWin + 1];
+    __shared__ int shi[2][kPtWin + 1];
+    __shared__ int s_x[2], s_w[2];  // window start label and width per ring (i, i + 1)
+    const double scale = fx_scale(dc);
+    // segment = (interval k, ring i, cells c0..c1), a geometry table
+    const int4 sg = segs[blockIdx.x];
+    const int k = sg.x, i = sg.y, c0 = sg.z, c1 = sg.w;
+    const int mti = __ldg(g.mtheta + i);
+    // label windows: ring i cells c0..c1+1; ring i+1 the same angular range
+    // (ratio mt'/mt, field-line skew over one interval) with a 2-label margin
+    if (threadIdx.x < 2) {
+        const int m = i + threadIdx.x, mt = __ldg(g.mtheta + m);
+        if (threadIdx.x == 0) {
+            s_x[0] = c0;
+            s_w[0] = min(c1 - c0 + 2, mt);
+        } else {
+            const double dq = (__ldg(g.qtinv + i) - __ldg(g.qtinv + m)) * kInvTwoPi;
+            const double z0 = (double)(g.k0 + k) * g.dzeta;
+            double f0 = (double)c0 / mti + z0 * dq - 2.0 / mt - g.dzeta * fabs(dq);
+            f0 -= floor(f0);
+            s_x[1] = min(max((int)floor(f0 * mt), 0), mt - 1);
+            const double span = (double)(c1 + 1 - c0) / mti + 4.0 / mt + 2.0 * g.dzeta * fabs(dq);
+            s_w[1] = min((int)ceil(span * mt) + 2, mt);
+        }
+    }
+    for (int e = threadIdx.x; e < 2 * (kPtWin + 1); e += blockDim.x) {
+        (&slo[0][0])[e] = 0u;
+        (&shi[0][0])[e] = 0;
+    }
+    __syncthreads();
+    const int W0 = s_w[0], W1 = s_w[1];
+    const bool fits = 2 * (W0 + W1) <= kPtWin;
+    const int cp = threadIdx.x & 1;  // twin copy of this thread (even / odd)
+    const int c = c0 + (int)threadIdx.x;
+    unsigned long long fb = 0;
+    if (c <= c1) {
+        const unsigned key = (unsigned)(k * g.mgrid + __ldg(g.igrid + i) + c);
+        for (unsigned e = offset[key]; e < offset[key + 1]; e++) {
+            const unsigned q = rec[e];
+            const long long p = q >> 2;
+            const int l = (int)(q & 3);
+            const double psi = ldp<R>(s.x[0], p), theta = ldp<R>(s.x[1], p), zeta = ldp<R>(s.x[2], p),
+                         w = ldp<R>(s.x[4], p), mu = ldp<R>(s.mu, p);
+            if (!isfinite((psi + theta + zeta + mu) * 0.0 + w)) continue;
+            double r, invB, rho, inv_r;
+            gyro_radius(g, psi, cos_theta(theta), mu, &r, &invB, &rho, &inv_r);
+            double wz1;
+            int kk = plane_of(g, zeta, &wz1) - g.k0;
+            kk = min(max(kk, 0), g.P - 1);
+            const double ws = __dmul_rn(w, scale);
+            const double wz[2] = {__dmul_rn(__dsub_rn(1.0, wz1), ws), __dmul_rn(wz1, ws)};
+            // this point only: the 2 rings x 2 label nodes x 2 planes
+            gyro_point(g, r, theta, zeta, rho, inv_r, l, [&](int m, int j, int mt, double a0, double a1) {
+                const int rr = m - i;  // 0 or 1 for this point's cell
+                const int j1 = (j + 1 == mt) ? 0 : j + 1;
+#pragma unroll
+                for (int pl = 0; pl < 2; pl++) {
+                    const long long v0 = fx_val(fx_magic(wz[pl], a0)), v1 = fx_val(fx_magic(wz[pl], a1));
+#pragma unroll
+                    for (int u = 0; u < 2; u++) {
+                        const int ju = u ? j1 : j;
+                        const long long v = u ? v1 : v0;
+                        if (!v) continue;
+                        const unsigned d = (rr == 0 || rr == 1) ? wrap_diff(ju, s_x[rr], mt) : 0xffffffffu;
+                        const int Wr = rr == 0 ? W0 : W1;
+                        if (fits && (unsigned)rr < 2u && d < (unsigned)Wr) {
+                            const int slot = pl * (W0 + W1) + (rr ? W0 : 0) + (int)d;
+                            atomicAdd(&slo[cp][slot], (unsigned)v & 0xffffu);
+                            atomicAdd(&shi[cp][slot], (int)(v >> 16));
+                        } else {
+                            red_i64(fx + fx_node(g, kk + pl, m, ju, mt), v);
+                            fb++;
+                        }
+                    }
+                }
+            });
+        }
+    }
+    __syncthreads();
+    if (fits)
+        for (int e = threadIdx.x; e < 2 * (W0 + W1); e += blockDim.x) {
+            const long long v = (long long)shi[0][e] * 65536 + (long long)slo[0][e] + (long long)shi[1][e] * 65536 +
+                                (long long)slo[1][e];
+            if (!v) continue;
+            const int pl = e / (W0 + W1), x = e - pl * (W0 + W1);
+            const int rr = x < W0 ? 0 : 1, d = rr ? x - W0 : x;
+            const int m = i + rr, mt = __ldg(g.mtheta + m);
+            int j = s_x[rr] + d;
+            if (j >= mt) j -= mt;
+            red_i64(fx + fx_node(g, k + pl, m, j, mt), v);
+        }
+    if (fb) atomicAdd((unsigned long long*)&dc->fallback, fb);
+}
+
+// host: point binning (keys, scan, scatter) + segmented twin-copy deposit
+void launch_deposit_points(const Geo& g, const PSet& s, long long n, long long* fx, DevCounters* dc, unsigned* pkey,
+                           unsigned* prank, unsigned* rec, unsigned* count, unsigned* offset, unsigned* scan_tmp,
+                           const int4* segs, int nseg, cudaStream_t st) {
+    if (n <= 0) return;
+    const long long nkeys = (long long)g.P * g.mgrid;
+    cudaMemsetAsync(count, 0, (nkeys + 1) * sizeof(unsigned), st);
+    const int blocks = (int)std::min<long long>((4 * n + 255) / 256, 148LL * 16);
+    if (g.prec32) k_point_keys<float><<<blocks, 256, 0, st>>>(g, s, n, pkey, prank, count);
+    else k_point_keys<double><<<blocks, 256, 0, st>>>(g, s, n, pkey, prank, count);
+    launch_scan_u32(count, offset, nkeys, scan_tmp, st);
+    k_point_scatter<<<blocks, 256, 0, st>>>(pkey, prank, offset, 4 * n, rec);
+    if (g.prec32) k_deposit_points<float><<<nseg, 256, 0, st>>>(g, s, offset, rec, segs, fx, dc);
+    else k_deposit_points<double><<<nseg, 256, 0, st>>>(g, s, offset, rec, segs, fx, dc);
+    g_launches += 3;
 }
 
 template <int NB>

@@ -267,3 +267,21 @@ def test_push_loop_fission_matches_fused(G, orc, Tcfg):
     o1, o2 = np.argsort(outs[0]["id"]), np.argsort(outs[1]["id"])
     for k in ("psi", "theta", "zeta", "rho", "w"):
         assert rel_err(outs[1][k][o2], outs[0][k][o1]) <= 1e-14, k
+
+
+@pytest.mark.parametrize("size,n", [("T", 12100), ("A", 300_000)])
+def test_update_binning_charge_ablation_bitwise(G, orc, size, n):
+    """charge mode 2 (the paper's update binning: points binned by
+    their own cell, one thread per super-cell, twin shared-memory copies) gives
+    the bitwise-identical fixed-point grid of the product deposit."""
+    cfg = synth.config(size)
+    parts = synth.load_particles(cfg, n, seed=17, w_amp=0.1)
+    grids = []
+    for mode in (0, 2):
+        ctx = ctx_for(G, size)
+        ctx.set_charge_mode(mode)
+        ctx.set_particles(parts)
+        ctx.charge()
+        grids.append(ctx.get_grid(G.GRID_CHARGE))
+        ctx.close()
+    assert np.array_equal(grids[0], grids[1])
