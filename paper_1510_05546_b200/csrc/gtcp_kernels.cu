@@ -1191,7 +1191,7 @@ __device__ __forceinline__ void push_epilogue(DevCounters* dc, double wmax, long
     if (nonfinite) dc->nonfinite = 1;
 }
 
-template <int MINB, bool CS, int GU = 8, class R = double, class FT = R, int MODE = 0>
+template <int MINB, bool CS, int GU = 8, class R = double, class FT = R, int MODE = 0, bool S1 = false>
 __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long long n, double h,
                                              const double* __restrict__ gf, DevCounters* dc,
                                              double* __restrict__ g3 = nullptr) {
@@ -1221,8 +1221,10 @@ __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long lon
             push_one<GU, FT, 2>(g, rt_dyn, ld(pp.src[0]), ld(pp.src[1]), ld(pp.src[2]), ld(pp.src[3]), ld(pp.src[4]),
                                 ld(pp.mu), base, h, gf, X, refl, clamps, gio);
         } else {
-            push_one<GU, FT>(g, rt_dyn, ld(pp.src[0]), ld(pp.src[1]), ld(pp.src[2]), ld(pp.src[3]), ld(pp.src[4]),
-                             ld(pp.mu), base, h, gf, X, refl, clamps);
+            // S1 (stage 1: X + dt/2 F(X)): the source is the base, read once
+            auto lds = [&](int d) { return S1 ? base[d] : ld(pp.src[d]); };
+            push_one<GU, FT>(g, rt_dyn, lds(0), lds(1), lds(2), lds(3), lds(4), ld(pp.mu), base, h, gf, X, refl,
+                             clamps);
         }
         // one test: a NaN or Inf in any component survives the product with 0
         if (!isfinite((X[0] + X[1] + X[2] + X[3]) * 0.0 + X[4])) nonfinite = 1;
@@ -1272,6 +1274,10 @@ void launch_push3(const Geo& g, const double* const src[5], const double* const 
         k_push<2, true, 8, double, double, 1><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc, g3);
         k_push<2, true, 8, double, double, 2><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc, g3);
         g_launches++;
+    } else if (src[0] == base[0]) {  // stage 1: the source is the base (read once)
+        if (g.prec32) k_push<2, true, 8, float, float, 0, true><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
+        else if (g.f32field) k_push<2, true, 8, double, float, 0, true><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
+        else k_push<2, true, 8, double, double, 0, true><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
     } else if (g.prec32) k_push<2, true, 8, float><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
     else if (g.f32field) k_push<2, true, 8, double, float><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
     else k_push<2, true, 8, double><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
