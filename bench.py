@@ -221,6 +221,8 @@ def run_gpu(args):
     assert ntor * args.nradial * args.npartdom == world, "GPUs must equal ntoroidal * nradial * npartdom"
     p = G.gtcp_default_params(size, ntoroidal=ntor, nradial=args.nradial, npartdom=args.npartdom,
                               bin_every=args.bin_every, precision=args.precision, **over)
+    if args.bin_mu:
+        p.bin_mu = args.bin_mu
     nccl_id = None
     if world > 1:
         obj = [G.gtcp_nccl_unique_id() if rank == 0 else None]
@@ -415,6 +417,7 @@ def main():
     ap.add_argument("--npartdom", type=int, default=1)
     ap.add_argument("--micell", type=int, default=None)
     ap.add_argument("--mzetamax", type=int, default=None)
+    ap.add_argument("--bin-mu", type=int, default=None)
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32])
     # ablations of the paper's own kernel designs
     ap.add_argument("--push-mode", type=int, default=0, choices=[0, 1])

@@ -110,7 +110,14 @@ static ncclResult_t loop_complete_recv(const Pending& p) {
         m = q.front();
         q.pop_front();
     }
-    if (m->bytes != p.bytes) return ncclInvalidUsage;  // NCCL: send/recv sizes must match
+    if (m->bytes != p.bytes) {  // NCCL: send/recv sizes must match; release the sender, report the misuse
+        {
+            std::lock_guard<std::mutex> lk(h->mu);
+            m->consumed = true;
+        }
+        h->cv.notify_all();
+        return ncclInvalidUsage;
+    }
     cudaError_t e = cudaStreamWaitEvent(p.st, m->ready, 0);
     if (e == cudaSuccess && p.bytes) e = cudaMemcpyAsync(p.buf, m->src, p.bytes, cudaMemcpyDeviceToDevice, p.st);
     cudaEvent_t d = nullptr;
