@@ -45,6 +45,18 @@ MUTATIONS = [
     ("field g_theta one-sided",
      "double gt = (pl[g.igrid[i] + (j + 1) % mt] - pl[g.igrid[i] + (j - 1 + mt) % mt]) / (2.0 * dth);",
      "double gt = (pl[g.igrid[i] + (j + 1) % mt] - pl[g.igrid[i] + j]) / dth;"),
+    ("push: weight drive sign flipped (-v_E,r kappa)",
+     "(vEr * kappa - (vpar * (B / p->R0) * gp + vdr * gr + vdt * gt / r));",
+     "(-vEr * kappa - (vpar * (B / p->R0) * gp + vdr * gr + vdt * gt / r));"),
+    ("push: mirror force dropped",
+     "double vdot = -mu * B * B * B * r * st / (q * p->R0 * p->R0);", "double vdot = 0.0;"),
+    ("push: dB/dtheta sign flipped",
+     "double dBdt = B * B * (r / p->R0) * st;", "double dBdt = -B * B * (r / p->R0) * st;"),
+    ("push: curvature drift without the mirror part (v_par^2 only)",
+     "double Cd = (vpar * vpar + mu * B) / (p->omega0 * p->R0);", "double Cd = (vpar * vpar) / (p->omega0 * p->R0);"),
+    ("push: kappa without the energy dependence",
+     "double kappa = orc_prof(r) * (p->rln + (Ekin - 1.5) * p->rlt) / p->R0;",
+     "double kappa = orc_prof(r) * (p->rln + p->rlt) / p->R0;"),
     ("field g_r neighbour rings at the same label (not physical theta)",
      "gr = (ring_interp(p, &g, pl, i + 1, th, zeta_k) -\n                          ring_interp(p, &g, pl, i - 1, th, zeta_k)) / (2.0 * dr);",
      "gr = (ring_interp(p, &g, pl, i + 1, j * TWO_PI / g.mtheta[i + 1], 0.0) -\n"
