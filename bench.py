@@ -407,7 +407,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--size", default=None)
-    ap.add_argument("--bin-every", type=int, default=2)
+    ap.add_argument("--bin-every", type=int, default=3)
     ap.add_argument("--ref-sample", type=int, default=16_000_000)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")

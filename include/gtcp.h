@@ -82,7 +82,7 @@ typedef struct {
                              * one (cell, plane) are further ordered by their mu quantile
                              * (Exp(1) quantiles) so that a warp shares gyroradii; 4 */
     int32_t precision;      /* 64: fp64 state; 32: fp32 state (class D), fp64 arithmetic */
-    int32_t bin_every;      /* bin by cell every bin_every steps; 2 */
+    int32_t bin_every;      /* bin by cell every bin_every steps; 3 */
     int32_t poisson_iters;  /* fixed weighted-Jacobi sweeps (F-2)              */
     int32_t paranl;         /* velocity-space nonlinearity on      */
     int32_t drifts;         /* 1; 0 = test-only drift-off flag                 */

@@ -243,7 +243,7 @@ extern "C" gtcp_status gtcp_default_params(char size, gtcp_params* out) {
     memset(&p, 0, sizeof(p));
     p.mpsi = mpsi; p.mthetamax = mth; p.mzetamax = mze; p.micell = micell;
     p.ntoroidal = 1; p.npartdom = 1; p.nradial = 1;
-    p.precision = 64; p.bin_every = 2; p.bin_mu = 4; p.poisson_iters = 20; p.paranl = 1; p.drifts = 1; p.track_ids = 0;
+    p.precision = 64; p.bin_every = 3; p.bin_mu = 4; p.poisson_iters = 20; p.paranl = 1; p.drifts = 1; p.track_ids = 0;
     p.a0 = 0.1; p.a1 = 0.9; p.R0 = 2.78; p.omega0 = 125.0 * mpsi / 90.0;
     p.q0 = 0.854; p.q2 = 2.184; p.rln = 2.2; p.rlt = 6.9; p.tau = 1.0; p.dt = 0.06;
     p.jacobi_omega = 1.0; p.w_init_amp = 1e-3; p.vcut = 5.0; p.capacity_factor = 1.0;
