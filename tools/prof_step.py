@@ -13,7 +13,7 @@ ap.add_argument("--size", default="A")
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--warmup", type=int, default=0)
 ap.add_argument("--charge-mode", type=int, default=0)
-ap.add_argument("--bin-every", type=int, default=2)
+ap.add_argument("--bin-every", type=int, default=3)
 ap.add_argument("--tag", default="")
 ap.add_argument("--micell", type=int, default=None)
 ap.add_argument("--bin-mu", type=int, default=None)

@@ -12,6 +12,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --no-e2e --no-cpu --steps 2 --warmup 3 > gpurun_out/ncu_launch_$TAG.log 2>&1
 echo "launch list rc=$?"
 timeout 300 python tools/prof_step.py --size A --steps 1 --warmup 1 > gpurun_out/prof_$TAG.log 2>&1 && \
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"k_deposit_tiled|k_push" -c 4 \
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"k_deposit_tiled|k_push" -s 1 -c 4 \
     -o gpurun_out/kernels_$TAG python tools/prof_step.py --size A --steps 1 --warmup 1 > gpurun_out/ncu_full_$TAG.log 2>&1
 echo "ncu full rc=$?"
