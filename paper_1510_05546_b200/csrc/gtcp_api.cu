@@ -353,6 +353,14 @@ static gtcp_status init_ctx(const gtcp_params* p, int rank, int nranks, const vo
     g.psi_hi = 0.5 * g.a1 * g.a1 * (1.0 - 1e-12);
     g.dzeta = GTCP_TWO_PI / p->mzetamax;
     g.rhoG = std::sqrt(2.0) / p->omega0;
+    // deposit tile windows: a label-drift margin of 1 cell since the bin and a
+    // radial band for gyroradii up to 3 thermal radii (~1 % of the markers, with
+    // v_perp > 3 v_th, redo some contributions through L2); measured best at A
+    // against drift 0.5 and bands of 3.5 and 4
+    g.drift_cells = 1.0;
+    g.rho_cut_th = 3.0;
+    if (const char* e = getenv("GTCP_DRIFT_CELLS")) g.drift_cells = std::max(0.0, atof(e));  // experiments
+    if (const char* e = getenv("GTCP_RHO_CUT")) g.rho_cut_th = std::max(1.0, atof(e));       // experiments
     g.inv_omega0 = 1.0 / p->omega0;
     g.inv_omega0_R0 = 1.0 / (p->omega0 * p->R0);
     g.nrad = nrad;

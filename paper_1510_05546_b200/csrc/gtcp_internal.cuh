@@ -33,6 +33,8 @@ struct Geo {
     double psi_lo, psi_hi;         // a0^2/2, a1^2/2 padded inwards: psi strictly inside needs no reflection test
     double dzeta;                  // 2 pi / mzetamax
     double rhoG;                   // sqrt(2) / omega0 (F-1)
+    double drift_cells;            // label-drift margin of the deposit tile windows (cells since the bin)
+    double rho_cut_th;             // radial band of the tile windows: gyroradii up to rho_cut_th thermal radii
     double inv_omega0, inv_omega0_R0;
     const int* mtheta;             // [mpsi+1]
     const int* igrid;              // [mpsi+2]

@@ -290,7 +290,7 @@ __device__ __forceinline__ double win_halfwidth(const Geo& g, int i, int c0, int
     double rm = g.a0 + m * g.dr;
     double thm = (m >= i - 1 && m <= i + 2) ? rho_cut / rm * kInvTwoPi : 0.0;
     *dq_out = dq;
-    return half0 + g.dzeta * fabs(dq) + thm + 1.0 / __ldg(g.mtheta + m);
+    return half0 + g.dzeta * fabs(dq) + thm + g.drift_cells / __ldg(g.mtheta + m);
 }
 
 __device__ __forceinline__ int win_width(const Geo& g, int i, int c0, int c1, int m, double rho_cut) {
@@ -309,7 +309,7 @@ __device__ __forceinline__ int win_nodes(const Geo& g, int i, int c0, int c1, do
     return S * (g.P + 1);
 }
 
-static double deposit_rho_cut(const Geo& g) { return 3.0 / g.omega0; }
+static double deposit_rho_cut(const Geo& g) { return g.rho_cut_th / g.omega0; }
 
 struct WinTables {
     int m_lo, nr, S, total;
