@@ -63,7 +63,7 @@ struct gtcp_ctx_s {
     long long* fx = nullptr;   // (P+1) * mgrid fixed-point charge
     double *rhoH = nullptr, *dnH = nullptr, *tmpH = nullptr, *phiH = nullptr;
     double *rhs = nullptr, *jphi = nullptr, *g1 = nullptr, *g2 = nullptr;
-    double* gfield = nullptr;  // P * mgrid * 6
+    double* gfield = nullptr;  // P * gstride * 6 (interval-interleaved gather layout)
     double* nm = nullptr;      // mpsi+1 marker density
     double* ringsum = nullptr; // mpsi+1
     double* phi00 = nullptr;   // 5 * (mpsi+1)
@@ -339,6 +339,17 @@ static gtcp_status init_ctx(const gtcp_params* p, int rank, int nranks, const vo
     Geo& g = c->geo;
     g.mpsi = M; g.mzetamax = p->mzetamax; g.P = P; g.k0 = c->k0; g.ntor = p->ntoroidal; g.rank_t = c->rank_t;
     g.mgrid = mg; g.paranl = p->paranl; g.drifts = p->drifts;
+    // gather-field interval stride: 3 (mod 8) nodes.  A 16-byte load of a
+    // quarter-warp costs one L1 wavefront per distinct line on each of the 8
+    // 16-byte chunk positions (tools/microbench/ldg256.cu); records are 48 B
+    // (3 chunks), so lanes at the same label in intervals k and k + d collide
+    // when 3 d gstride = 0 (mod 8).  3 mod 8 keeps d = 1, 2 apart (mgrid itself
+    // is 1 mod 8 at class A: neighbouring labels across an interval collided).
+    g.gstride = mg + ((3 - mg % 8) + 8) % 8;
+    if (const char* e = getenv("GTCP_GSTRIDE_RES")) {  // experiments: residue mod 8, or -1 for mgrid
+        const int r = atoi(e);
+        g.gstride = r < 0 ? mg : mg + ((r - mg % 8) % 8 + 8) % 8;
+    }
     g.prec32 = (p->precision == 32);
     g.f32field = g.prec32 || p->field_f32 != 0;
     gtcp::g_prec32 = g.prec32;
@@ -456,8 +467,8 @@ static gtcp_status init_ctx(const gtcp_params* p, int rank, int nranks, const vo
     CU(dalloc(&c->jphi, (long long)P * mg));
     CU(dalloc(&c->g1, (long long)P * mg));
     CU(dalloc(&c->g2, (long long)P * mg));
-    CU(dalloc(&c->gfield, (long long)P * mg * 6));
-    CU(cudaMemset(c->gfield, 0, (long long)P * mg * 6 * sizeof(double)));
+    CU(dalloc(&c->gfield, (long long)P * c->geo.gstride * 6));
+    CU(cudaMemset(c->gfield, 0, (long long)P * c->geo.gstride * 6 * sizeof(double)));
     CU(dalloc(&c->nm, M + 1));
     CU(dalloc(&c->ringsum, M + 1));
     CU(dalloc(&c->phi00, 5 * (M + 1)));

@@ -401,11 +401,11 @@ __global__ void k_field(Geo g, const double* __restrict__ phiH, FT* __restrict__
         double gt = (pl[ig + jp] - pl[ig + jm]) / (2.0 * dth);
         double gp = (pl[g.mgrid + ig + j] - pl[-(long long)g.mgrid + ig + j]) * inv2dz;
         if (k < g.P) {
-            FT* o = gf + ((long long)k * g.mgrid + node) * 6;
+            FT* o = gf + ((long long)k * g.gstride + node) * 6;
             o[0] = (FT)gr; o[1] = (FT)gt; o[2] = (FT)gp;
         }
         if (k > 0) {
-            FT* o = gf + ((long long)(k - 1) * g.mgrid + node) * 6 + 3;
+            FT* o = gf + ((long long)(k - 1) * g.gstride + node) * 6 + 3;
             o[0] = (FT)gr; o[1] = (FT)gt; o[2] = (FT)gp;
         }
     }
@@ -424,8 +424,8 @@ __global__ void k_gfield_export(Geo g, const FT* __restrict__ gf, double* __rest
     long long total = (long long)(g.P + 1) * g.mgrid;
     GRID_LOOP(e, total) {
         int k = (int)(e / g.mgrid), node = (int)(e % g.mgrid);
-        const FT* s = (k < g.P) ? gf + ((long long)k * g.mgrid + node) * 6
-                                : gf + ((long long)(k - 1) * g.mgrid + node) * 6 + 3;
+        const FT* s = (k < g.P) ? gf + ((long long)k * g.gstride + node) * 6
+                                : gf + ((long long)(k - 1) * g.gstride + node) * 6 + 3;
         out[e * 3 + 0] = s[0];
         out[e * 3 + 1] = s[1];
         out[e * 3 + 2] = s[2];
@@ -446,8 +446,8 @@ __global__ void k_gfield_import(Geo g, const double* __restrict__ in, FT* __rest
         int k = (int)(e / g.mgrid), node = (int)(e % g.mgrid);
         for (int c = 0; c < 3; c++) {
             double v = in[e * 3 + c];
-            if (k < g.P) gf[((long long)k * g.mgrid + node) * 6 + c] = (FT)v;
-            if (k > 0) gf[((long long)(k - 1) * g.mgrid + node) * 6 + 3 + c] = (FT)v;
+            if (k < g.P) gf[((long long)k * g.gstride + node) * 6 + c] = (FT)v;
+            if (k > 0) gf[((long long)(k - 1) * g.gstride + node) * 6 + 3 + c] = (FT)v;
         }
     }
 }

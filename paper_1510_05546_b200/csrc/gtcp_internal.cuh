@@ -25,6 +25,7 @@ struct Geo {
     double rbound[9];              // radial domain boundaries r(b_0 = ring 0) .. r(b_nrad = ring mpsi)
     double rbound2[9];             // their squares (fast classification away from a boundary)
     int mgrid;                     // nodes per plane incl. duplicates (< 2^31)
+    int gstride;                   // nodes per interval of the push's gather field (mgrid padded to 3 mod 8)
     int paranl, drifts;
     int prec32;                    // particle store in fp32 (arithmetic stays fp64)
     int f32field;                  // gather field stored in fp32 (precision 32, or field_f32)

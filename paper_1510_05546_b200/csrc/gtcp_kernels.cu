@@ -411,8 +411,8 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
             __syncthreads();
             int S = 0;
             for (int q = 0; q < nr; q++) S += T.WO[q].x + 1;  // column W of each ring: its trash column
-            // pad the plane stride to 16 (mod 32) words: the lane bit that picks
-            // plane k or k+1 then always flips the shared-memory bank half
+            // pad the plane stride to kPlanePad (mod 32) words (4: measured best
+            // of the bank-model candidates)
             S += (kPlanePad - (S & 31) + 32) & 31;
             const bool fits = S * P1 <= cap_nodes;  // else: everything via L2
             __syncthreads();
@@ -1095,7 +1095,7 @@ __device__ __forceinline__ void push_one(const Geo& g, const RingTab* __restrict
     // bounding plane accumulated separately, plane weights and 1/4 applied once
     double r0 = 0.0, t0 = 0.0, p0 = 0.0, r1 = 0.0, t1 = 0.0, p1 = 0.0;
     using V2 = typename std::conditional<std::is_same<FT, float>::value, float2, double2>::type;
-    const FT* gk = reinterpret_cast<const FT*>(gf) + (long long)k * g.mgrid * 6;
+    const FT* gk = reinterpret_cast<const FT*>(gf) + (long long)k * g.gstride * 6;
 #pragma unroll GU
     for (int q = 0; q < 8; q++) {
         const V2* qq = reinterpret_cast<const V2*>(gk + (long long)node[q] * 6);
@@ -1726,7 +1726,7 @@ __global__ void k_heat_flux(Geo g, PSet s, long long n, const double* __restrict
         k = min(max(k, 0), g.P - 1);
         const double wz0 = 1.0 - wz1;
         double gt = 0.0;
-        const FT* gk = gff + (long long)k * g.mgrid * 6;
+        const FT* gk = gff + (long long)k * g.gstride * 6;
         gyro_stencil(g, r, theta, zeta, rho, inv_r, [&](int m, int j, int mt, double a0, double a1) {
             const FT* rj = gk + ((long long)__ldg(g.igrid + m) + j) * 6;  // nodes j, j + 1 (duplicate at mt)
             gt += a0 * (wz0 * (double)rj[1] + wz1 * (double)rj[4]) + a1 * (wz0 * (double)rj[7] + wz1 * (double)rj[10]);

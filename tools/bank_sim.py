@@ -94,7 +94,7 @@ def build(size, mzetamax, ring_frac, tile_max, nmu, seed, layout):
         S += W[q] + 1 + layout.get("ring_gap", 0)
         if layout.get("ring_align"):
             S += (-S) % layout["ring_align"]
-    pad = layout.get("pad", 16)
+    pad = layout.get("pad", 4)  # kPlanePad of the kernel (GTCP_PLANE_PAD)
     if pad is not None:
         S += (pad - (S & 31) + 32) & 31
     return dict(n=n, r=r, zeta=zeta, theta=theta, rho=rho, K=K, mt=mt, qt=qt, a0=a0, a1=a1, dr=dr, M=M,
@@ -164,7 +164,7 @@ if __name__ == "__main__":
     ap.add_argument("--nmu", type=int, default=4)
     a = ap.parse_args()
     for frac in (0.3, 0.6, 0.9):
-        T = build(a.size, a.mzetamax, frac, 8192, a.nmu, 1, {"pad": 16})
+        T = build(a.size, a.mzetamax, frac, 8192, a.nmu, 1, {"pad": 4})
         print(f"ring {frac:.1f}: S={T['S']} nr={T['nr']} W={list(T['W'])} wavefronts/ATOMS rot={run(T):.2f} "
               f"norot={run(T, rot=False):.2f}")
 

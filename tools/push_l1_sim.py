@@ -1,14 +1,16 @@
-"""CPU model of k_push's gather on the L1 data pipe: one wavefront per
-distinct 128-byte line per quarter-warp of every warp-wide LDG.128
-(DESIGN.md §7.3).  Builds cell-sorted markers of the paper's density on the
+"""CPU model of k_push's gather on the L1 data pipe: a
+quarter-warp of a warp-wide LDG.128 takes one wavefront per distinct 128-byte
+line on each of the 8 sixteen-byte chunk positions of a line (address bits
+4-6; measured with tools/microbench/ldg256.cu).  Builds cell-sorted markers of the paper's density on the
 class-A grid (bin key order of H-4 with the mu sub-bins), ages them by
 `--age` RK2 half-steps of parallel streaming, and counts the wavefronts of
 the 6 x 8 gather loads per marker for field-record layouts:
-  interleaved48 : node n of interval k at 48 * (k mgrid + n), pair j, j+1 = 96 B
+  interleaved48 : node n of interval k at 48 * (k gstride + n), pair j, j+1 = 96 B
+                  (gstride = mgrid padded to --gstride-res mod 8; -1: mgrid)
   pair128       : the pair (j, j+1) of interval k as one 128-byte line
   interleaved48_f32 / pair64_f32 : the same in fp32 (3 LDG.128 per pair)
 
-  python tools/push_l1_sim.py --size A --ncell 400 --age 1
+  python tools/push_l1_sim.py --size A --ncell 400 --age 1 --gstride-res 3
 """
 import argparse
 import math
@@ -58,10 +60,12 @@ def markers(size, ncell_ring, seed, age, nmu=4):
     return p, geo, r[o], theta[o], zeta[o], mu[o], B[o]
 
 
-def records(p, geo, r, theta, zeta, mu, B):
-    """Per marker the 8 (point, ring) global node-pair indices (k mgrid + igrid_m + j)."""
+def records(p, geo, r, theta, zeta, mu, B, res=3):
+    """Per marker the 8 (point, ring) global node-pair indices (k gstride + igrid_m + j)."""
     mt, ig, qt = geo["mtheta"], geo["igrid"], geo["qtinv"]
     M, K, mg = p.mpsi, p.mzetamax, geo["mgrid"]
+    if res >= 0:
+        mg += ((res - mg % 8) % 8 + 8) % 8
     dr = (p.a1 - p.a0) / M
     rho = np.sqrt(2 * mu / B) / p.omega0
     k = np.minimum(np.floor(zeta * K / TWO_PI).astype(int), K - 1)
@@ -94,11 +98,19 @@ def wavefronts(rec, layout):
         base, nchunk = rec * 64, 3
     tot = 0
     for c in range(nchunk):
-        lines = (base + 16 * c) // 128  # [warps, 32, 8]
+        addr = base + 16 * c  # [warps, 32, 8]
+        lines, pos = addr // 128, (addr // 16) % 8
         for qw in range(4):
-            q = lines[:, 8 * qw:8 * qw + 8, :]  # [warps, 8 lanes, 8 records]
-            s = np.sort(q, axis=1)
-            tot += int((1 + (np.diff(s, axis=1) != 0).sum(axis=1)).sum())
+            ql = lines[:, 8 * qw:8 * qw + 8, :]  # [warps, 8 lanes, 8 records]
+            qp = pos[:, 8 * qw:8 * qw + 8, :]
+            worst = np.zeros(ql.shape[0:1] + ql.shape[2:], np.int64)
+            for b in range(8):  # distinct lines on chunk position b
+                key = np.where(qp == b, ql, -1)
+                srt = np.sort(key, axis=1)
+                nd = (np.diff(srt, axis=1) != 0) & (srt[:, 1:] >= 0)
+                cnt = nd.sum(axis=1) + (srt[:, 0] >= 0)
+                worst = np.maximum(worst, cnt)
+            tot += int(worst.sum())
     nldg = rec.shape[0] * 8 * nchunk
     return tot / nldg, tot / rec.shape[0]
 
@@ -108,9 +120,10 @@ def main():
     ap.add_argument("--size", default="A")
     ap.add_argument("--ncell", type=int, default=400)
     ap.add_argument("--age", type=float, default=1.0)
+    ap.add_argument("--gstride-res", type=int, default=3, help="interval stride residue mod 8 (-1: mgrid)")
     a = ap.parse_args()
     p, geo, *st = markers(a.size, a.ncell, 1, a.age)
-    rec = records(p, geo, *st)
+    rec = records(p, geo, *st, res=a.gstride_res)
     for lay in ("interleaved48", "pair128", "interleaved48_f32", "pair64_f32"):
         per_ldg, per_warp = wavefronts(rec, lay)
         print(f"{lay:18s} {per_ldg:5.2f} wavefronts per LDG.128, {per_warp:6.1f} per warp-marker")
