@@ -17,7 +17,9 @@ from test_gpu_parity import G, TOL, ctx_for, rel_err, circ  # noqa: F401
 pytestmark = pytest.mark.gpu
 TWO_PI = 2 * math.pi
 
-GEOMS = [("A", dict(mzetamax=4)), ("D", dict(mzetamax=2, poisson_iters=3))]
+# T with 3 planes: an odd plane count (the gyro-average kernels do 2 planes
+# per thread, the last group has one)
+GEOMS = [("A", dict(mzetamax=4)), ("D", dict(mzetamax=2, poisson_iters=3)), ("T", dict(mzetamax=3))]
 
 
 def _charge_input(orc, cfg, p, n, seed):
@@ -25,7 +27,7 @@ def _charge_input(orc, cfg, p, n, seed):
     return parts, orc.charge_global(p, parts), orc.marker_norm(p, parts)
 
 
-@pytest.mark.parametrize("size,over", GEOMS, ids=[g[0] for g in GEOMS])
+@pytest.mark.parametrize("size,over", GEOMS, ids=[g[0] + str(g[1]["mzetamax"]) for g in GEOMS])
 def test_poisson_smooth_parity_at_scale(G, orc, size, over):
     cfg = synth.config(size, **over)
     p = orc.make_params(cfg)
@@ -41,7 +43,7 @@ def test_poisson_smooth_parity_at_scale(G, orc, size, over):
     ctx.close()
 
 
-@pytest.mark.parametrize("size,over", GEOMS, ids=[g[0] for g in GEOMS])
+@pytest.mark.parametrize("size,over", GEOMS, ids=[g[0] + str(g[1]["mzetamax"]) for g in GEOMS])
 def test_field_parity_at_scale(G, orc, size, over):
     """Gradient of a potential with structure on every ring and plane (a
     drift-wave-like mode plus noise, smoothed), through the seam."""
