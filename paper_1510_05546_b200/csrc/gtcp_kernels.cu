@@ -1002,6 +1002,12 @@ struct PushPtrs {
     unsigned* cntR;
 };
 
+#ifndef GTCP_PUSH_MINB  // experiment builds: CTAs per SM / gather unroll of the fp64 push
+#define GTCP_PUSH_MINB 2
+#endif
+#ifndef GTCP_PUSH_GU
+#define GTCP_PUSH_GU 8
+#endif
 static constexpr int kShiftChunkLog2 = 14;  // == log2(kChunk) of gtcp_shift.cu
 
 // same expression as the shift's classify (mode 0): destination toroidal domain
@@ -1277,10 +1283,10 @@ void launch_push3(const Geo& g, const double* const src[5], const double* const 
     } else if (src[0] == base[0]) {  // stage 1: the source is the base (read once)
         if (g.prec32) k_push<2, true, 8, float, float, 0, true><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
         else if (g.f32field) k_push<2, true, 8, double, float, 0, true><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
-        else k_push<2, true, 8, double, double, 0, true><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
+        else k_push<GTCP_PUSH_MINB, true, GTCP_PUSH_GU, double, double, 0, true><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
     } else if (g.prec32) k_push<2, true, 8, float><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
     else if (g.f32field) k_push<2, true, 8, double, float><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
-    else k_push<2, true, 8, double><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
+    else k_push<GTCP_PUSH_MINB, true, GTCP_PUSH_GU, double><<<blocks, 256, smr, st>>>(g, pp, n, h, gfield, dc);
     g_launches++;
 }
 
