@@ -325,6 +325,18 @@ def run_gpu(args):
             roof["charge_deposit"]["smem_atomic"] = {
                 "achieved_wavefronts_per_s": ach, "peak_wavefronts_per_s": peak_wf, "frac": ach / peak_wf,
                 "wavefronts_per_launch": wf, "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom"}
+        # both kernels' own roof: the L1/shared data pipe (one wavefront per clock
+        # per SM), all its wavefronts (global gathers, shared atomics and loads)
+        for kern in ("charge_deposit", "push"):
+            wfa = tr.get(size, {}).get(kern, {}).get("l1_data_pipe_wavefronts_per_launch")
+            if wfa and kern in roof:
+                props = torch.cuda.get_device_properties(local)
+                clk_hz = (clk.summary() or {}).get("sm_mhz") or 1965.0
+                peak_wf = props.multi_processor_count * clk_hz * 1e6
+                ach = wfa / (roof[kern]["avg_ms"] * 1e-3)
+                roof[kern]["l1_data_pipe"] = {
+                    "achieved_wavefronts_per_s": ach, "peak_wavefronts_per_s": peak_wf, "frac": ach / peak_wf,
+                    "wavefronts_per_launch": wfa, "source": "ncu l1tex__data_pipe_lsu_wavefronts (lgds + shared)"}
     except Exception:
         pass
     # end to end through the C ABI with HOST buffers (pinned): H2D state, step, D2H state
