@@ -234,6 +234,8 @@ def run_gpu(args):
         ctx.set_push_mode(args.push_mode)  # ablation: loop fission
     if args.charge_mode:
         ctx.set_charge_mode(args.charge_mode)  # ablation: global-atomic deposit
+    if args.fused:
+        ctx.set_fused(True)  # push + next-stage deposit in one kernel
     ctx.load()
     info = ctx.get_info()
     n_local = info.n_local
@@ -434,6 +436,7 @@ def main():
     # ablations of the paper's own kernel designs
     ap.add_argument("--push-mode", type=int, default=0, choices=[0, 1])
     ap.add_argument("--charge-mode", type=int, default=0, choices=[0, 1, 2])
+    ap.add_argument("--fused", action="store_true", help="fused stage pipeline (one rank only)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -295,6 +295,17 @@ gtcp_status gtcp_set_charge_mode(gtcp_ctx ctx, int mode);
  * gyro-averaged gradient (3 doubles per particle) to HBM, an update kernel
  * reads it (fp64 state only; other precisions stay fused).  Same results. */
 gtcp_status gtcp_set_push_mode(gtcp_ctx ctx, int mode);
+/* SURVEY §8(f) #1, fused stage pipeline: 1 = gtcp_step pushes each RK2 stage
+ * and deposits the NEXT stage's charge from the new state in one kernel over
+ * the bin's tiles (no re-read of the state for the charge, one launch less);
+ * 0 = separate push and charge (default).  One rank, tiled charge, fp64 state
+ * only (GTCP_EINVAL otherwise); applies inside gtcp_step, the first charge of
+ * each gtcp_step call after gtcp_load / set_particles / step_host / set_grid
+ * is deposited separately.  The fused charge uses one bit less fixed-point
+ * scale (the new max|w| is not known before it is deposited); results match
+ * the unfused step within the fixed-point rounding (2^-31 of max|w|/4 per
+ * contribution). */
+gtcp_status gtcp_set_fused(gtcp_ctx ctx, int on);
 
 #ifdef __cplusplus
 }

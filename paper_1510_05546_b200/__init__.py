@@ -75,7 +75,7 @@ SYMBOLS = ("gtcp_default_params", "gtcp_geometry", "gtcp_nccl_unique_id", "gtcp_
            "gtcp_poisson_smooth", "gtcp_field", "gtcp_push", "gtcp_shift", "gtcp_bin", "gtcp_step",
            "gtcp_step_host", "gtcp_get_grid", "gtcp_set_grid", "gtcp_stats", "gtcp_timings", "gtcp_timings_reset",
            "gtcp_set_timing", "gtcp_set_charge_mode", "gtcp_sample_particles", "gtcp_loopback_create",
-           "gtcp_loopback_destroy", "gtcp_init_loopback", "gtcp_diag", "gtcp_set_push_mode")
+           "gtcp_loopback_destroy", "gtcp_init_loopback", "gtcp_diag", "gtcp_set_push_mode", "gtcp_set_fused")
 
 _lib = None
 
@@ -122,6 +122,7 @@ def lib():
             "gtcp_set_timing": (st, [vp, C.c_int]),
             "gtcp_set_charge_mode": (st, [vp, C.c_int]),
             "gtcp_set_push_mode": (st, [vp, C.c_int]),
+            "gtcp_set_fused": (st, [vp, C.c_int]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -336,6 +337,9 @@ class Context:
 
     def set_push_mode(self, mode: int):
         self._chk(lib().gtcp_set_push_mode(self._h, mode), "set_push_mode")
+
+    def set_fused(self, on: bool):
+        self._chk(lib().gtcp_set_fused(self._h, int(bool(on))), "set_fused")
 
 
 class LoopbackHub:

@@ -96,6 +96,9 @@ struct gtcp_ctx_s {
     // charge config
     int charge_mode = 0;
     int push_mode = 0;          // 1: loop-fission ablation of the push
+    int fused = 0;              // gtcp_set_fused: push + next-stage deposit in one kernel
+    int fused_ctas = 0;
+    int fx_pending = 0;         // RK2 stage whose charge the last fused push already deposited into fx (0: none)
     // charge mode 2 (update-binning ablation): point records and segments
     unsigned *pkey = nullptr, *prank = nullptr, *prec = nullptr;
     int4* psegs = nullptr;
@@ -809,8 +812,14 @@ static gtcp_status compute_marker_norm(gtcp_ctx c) {
     return GTCP_OK;
 }
 
+static gtcp_status charge_impl(gtcp_ctx c);
 extern "C" gtcp_status gtcp_charge(gtcp_ctx c) {
     CHECK_CTX(c);
+    c->fx_pending = 0;
+    return charge_impl(c);
+}
+
+static gtcp_status charge_impl(gtcp_ctx c) {
     {
         PhaseTimer t(c, GTCP_T_CHARGE);
         gtcp_status s = deposit_fx(c);
@@ -907,8 +916,49 @@ static void push_range(gtcp_ctx c, double* const* src, double* const* base, doub
                      fuse ? cntL : nullptr, fuse ? cntR : nullptr, c->push_mode == 1 ? c->g3 : nullptr);
 }
 
+static gtcp_status push_impl(gtcp_ctx c, int stage);
 extern "C" gtcp_status gtcp_push(gtcp_ctx c, int stage) {
     CHECK_CTX(c);
+    c->fx_pending = 0;
+    return push_impl(c, stage);
+}
+
+// can this stage's push also deposit the next stage's charge?
+static bool fused_ok(gtcp_ctx c) {
+    return c->fused && c->fused_ctas > 0 && c->nranks == 1 && c->charge_mode == 0 && c->push_mode == 0 &&
+           !c->geo.prec32 && !c->geo.f32field && c->n_binned == c->n && c->n > 0;
+}
+
+// the fused stage: X <- X + h F (as push_impl) and, from the new state in
+// registers, the fixed-point charge of the next RK2 stage.  Its scale F
+// follows the pre-push max|w| with one bit of headroom (the new weights are
+// not known before the deposit; |w| may grow within a stage).
+static gtcp_status push_fused(gtcp_ctx c, int stage) {
+    if (stage != c->stage_next) return set_err(c, GTCP_ESTATE, "push: unexpected RK2 stage");
+    PhaseTimer t(c, GTCP_T_PUSH);
+    launch_fx_scale(c->dc, c->st, 1);
+    CU(cudaMemsetAsync(c->fx, 0, (size_t)(c->P + 1) * c->mgrid * sizeof(long long), c->st));
+    CU(cudaMemsetAsync(&c->dc->wmax_bits, 0, 8, c->st));
+    double* src[5];
+    double* base[5];
+    double* out[5];
+    const double h = stage == 1 ? 0.5 * c->prm.dt : c->prm.dt;
+    for (int d = 0; d < 5; d++) {
+        src[d] = c->live[d];
+        base[d] = stage == 1 ? c->live[d] : c->saved[d];
+        out[d] = c->saved[d];
+    }
+    launch_push_deposit(c->geo, live_set(c), c->n, c->tiles, c->fx, c->dc, c->fused_ctas, c->dep_cap_nodes, src, base,
+                        out, c->gfield, h, c->st);
+    for (int d = 0; d < 5; d++) std::swap(c->live[d], c->saved[d]);
+    c->stage_next = stage == 1 ? 2 : 1;
+    c->fx_pending = c->stage_next;
+    CU(cudaMemcpyAsync(c->h_nonfinite, &c->dc->nonfinite, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    KCHECK();
+    return GTCP_OK;
+}
+
+static gtcp_status push_impl(gtcp_ctx c, int stage) {
     if (stage != c->stage_next) return set_err(c, GTCP_ESTATE, "push: unexpected RK2 stage");
     PhaseTimer t(c, GTCP_T_PUSH);
     CU(cudaMemsetAsync(&c->dc->wmax_bits, 0, 8, c->st));
@@ -1051,10 +1101,17 @@ extern "C" gtcp_status gtcp_step(gtcp_ctx c, int nsteps) {
     for (int s = 0; s < nsteps; s++) {
         for (int stage = 1; stage <= 2; stage++) {
             gtcp_status r;
-            if ((r = gtcp_charge(c)) != GTCP_OK) return r;
+            if (c->fx_pending == stage) {  // deposited by the previous (fused) push
+                PhaseTimer t(c, GTCP_T_CHARGE_RED);
+                r = charge_reduce(c);
+            } else {
+                r = charge_impl(c);
+            }
+            c->fx_pending = 0;
+            if (r != GTCP_OK) return r;
             if ((r = gtcp_poisson_smooth(c)) != GTCP_OK) return r;
             if ((r = gtcp_field(c)) != GTCP_OK) return r;
-            if ((r = gtcp_push(c, stage)) != GTCP_OK) return r;
+            if ((r = fused_ok(c) ? push_fused(c, stage) : push_impl(c, stage)) != GTCP_OK) return r;
             if ((r = gtcp_shift(c)) != GTCP_OK) return r;
         }
         // the push raises a device flag on a non-finite state; its
@@ -1099,6 +1156,7 @@ extern "C" gtcp_status gtcp_load(gtcp_ctx c) {
                           std::min<long long>(c->rank_p, n_rad % p.npartdom);
     c->n = n;
     c->stage_next = 1;
+    c->fx_pending = 0;
     CU(reset_nonfinite(c));
     PSet s = live_set(c);
     const double zlo = c->k0 * (GTCP_TWO_PI / p.mzetamax), zhi = (c->k0 + c->P) * (GTCP_TWO_PI / p.mzetamax);
@@ -1126,6 +1184,7 @@ extern "C" gtcp_status gtcp_set_particles(gtcp_ctx c, int64_t n, const double* c
     if (c->id && id) CU(cudaMemcpyAsync(c->id, id, n * sizeof(uint64_t), cudaMemcpyHostToDevice, c->st));
     c->n = n;
     c->stage_next = 1;
+    c->fx_pending = 0;
     CU(reset_nonfinite(c));
     gtcp_status r = do_bin(c);
     if (r != GTCP_OK) return r;
@@ -1193,6 +1252,7 @@ extern "C" gtcp_status gtcp_step_host(gtcp_ctx c, int64_t n, int64_t cap, double
     CU(upload_reals(c, c->mu, attr[5], n));
     c->n = n;
     c->stage_next = 1;
+    c->fx_pending = 0;  // a foreign state: the next charge is deposited afresh
     // the tiles of the last bin stay: they are exact for a state returned by
     // the previous step_host (same order); for any other order the deposit's
     // out-of-window path keeps the charge exact (slower)
@@ -1249,6 +1309,7 @@ extern "C" gtcp_status gtcp_get_grid(gtcp_ctx c, int which, int64_t cap, double*
 
 extern "C" gtcp_status gtcp_set_grid(gtcp_ctx c, int which, int64_t n, const double* host) {
     CHECK_CTX(c);
+    c->fx_pending = 0;
     const long long mg = c->mgrid;
     const long long planes = c->P + 1;
     if (!host) return set_err(c, GTCP_EINVAL, "set_grid: null buffer");
@@ -1389,11 +1450,31 @@ extern "C" gtcp_status gtcp_set_push_mode(gtcp_ctx c, int mode) {
     if (mode != 0 && mode != 1) return GTCP_EINVAL;
     if (mode == 1 && !c->g3) CU(dalloc(&c->g3, 3 * c->cap));
     c->push_mode = mode;
+    c->fx_pending = 0;
+    return GTCP_OK;
+}
+
+extern "C" gtcp_status gtcp_set_fused(gtcp_ctx c, int on) {
+    CHECK_CTX(c);
+    if (on != 0 && on != 1) return GTCP_EINVAL;
+    c->fx_pending = 0;
+    if (on && !c->fused_ctas) {
+        if (c->nranks != 1 || c->charge_mode != 0 || c->geo.prec32 || c->geo.f32field || c->dep_cap_nodes == 0)
+            return set_err(c, GTCP_EINVAL, "set_fused: one rank, tiled charge, fp64 state only");
+        const int per_sm = gtcp::configure_push_deposit(c->geo);
+        if (per_sm < 1) return set_err(c, GTCP_EINVAL, "set_fused: the fused kernel does not fit an SM");
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        c->fused_ctas = nsm * per_sm;
+    }
+    c->fused = on;
     return GTCP_OK;
 }
 
 extern "C" gtcp_status gtcp_set_charge_mode(gtcp_ctx c, int mode) {
     CHECK_CTX(c);
+    c->fx_pending = 0;
     if (mode < 0 || mode > 2) return GTCP_EINVAL;
     if (mode == 2 && !c->pkey) {
         // point records (4 per particle) and the (interval, ring, 256-cell) segments

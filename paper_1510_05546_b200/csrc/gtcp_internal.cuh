@@ -99,6 +99,13 @@ void launch_deposit_tiled(const Geo& g, const PSet& s, long long n, const Tile* 
 cudaError_t configure_deposit_tiled(size_t smem_bytes, int nb);
 size_t deposit_tiled_smem(int P, int nb);
 int deposit_tiled_ctas_per_sm(size_t smem_bytes, int nb);  // after configure_deposit_tiled
+// fused RK2 stage push + deposit of the next stage's charge;
+// configure returns the CTAs per SM it runs at (0: not available)
+size_t push_deposit_smem(const Geo& g, size_t* rt_off);
+int configure_push_deposit(const Geo& g);
+void launch_push_deposit(const Geo& g, const PSet& s, long long n, const Tile* tiles, long long* fx, DevCounters* dc,
+                         int ctas, int cap_nodes, const double* const src[5], const double* const base[5],
+                         double* const out[5], const double* gf, double h, cudaStream_t st);
 void launch_deposit_direct(const Geo& g, const PSet& s, long long begin, long long n, long long* fx,
                            DevCounters* dc, cudaStream_t st);
 // charge ablation: the paper's update-binning deposit (points binned by cell
@@ -106,7 +113,7 @@ void launch_deposit_direct(const Geo& g, const PSet& s, long long begin, long lo
 void launch_deposit_points(const Geo& g, const PSet& s, long long n, long long* fx, DevCounters* dc, unsigned* pkey,
                            unsigned* prank, unsigned* rec, unsigned* count, unsigned* offset, unsigned* scan_tmp,
                            const int4* segs, int nseg, cudaStream_t st);
-void launch_fx_scale(DevCounters* dc, cudaStream_t st);
+void launch_fx_scale(DevCounters* dc, cudaStream_t st, int headroom = 0);
 void launch_fx_to_real(const Geo& g, const long long* fx, double* rho, const DevCounters* dc, int planes,
                        cudaStream_t st);
 void launch_push3(const Geo& g, const double* const src[5], const double* const base[5], double* const out[5],

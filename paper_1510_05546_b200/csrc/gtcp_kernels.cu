@@ -205,13 +205,13 @@ __device__ __forceinline__ void stp_cs(double* a, long long p, double v) { __stc
 // |w| 2^F < 2^33 and every contribution (<= |w|/4) rounds to an integer of
 // magnitude below 2^31 (31-bit contributions; precision analysis DESIGN.md §3).
 // ---------------------------------------------------------------------------
-__global__ void k_fx_scale(DevCounters* dc) {
+__global__ void k_fx_scale(DevCounters* dc, int headroom) {
     double wmax = __longlong_as_double((long long)dc->wmax_bits);
     int F = 33;
     if (wmax > 0.0 && isfinite(wmax)) {
         int e;
         frexp(wmax, &e);  // wmax in [2^(e-1), 2^e)
-        F = 33 - e;
+        F = 33 - e - headroom;
     }
     F = max(-60, min(F, 60));
     dc->fx_shift = F;
@@ -219,8 +219,8 @@ __global__ void k_fx_scale(DevCounters* dc) {
     dc->tile_next = 0;
 }
 
-void launch_fx_scale(DevCounters* dc, cudaStream_t st) {
-    k_fx_scale<<<1, 1, 0, st>>>(dc);
+void launch_fx_scale(DevCounters* dc, cudaStream_t st, int headroom) {
+    k_fx_scale<<<1, 1, 0, st>>>(dc, headroom);
     g_launches++;
 }
 
@@ -368,11 +368,35 @@ extern "C" int gtcp_debug_addr_dump(unsigned* host) {
 }
 #endif
 
-template <class R, int NB>
+// SURVEY §8(f) #1, fused stage pipeline (an option, gtcp_set_fused): the
+// push of one RK2 stage and the deposit of the NEXT stage's charge in one
+// persistent kernel over the bin's tiles -- each marker is pushed (same
+// push_one as k_push) and its new position deposited straight from registers,
+// so the deposit's 40 B/particle re-read of the state and one launch go away.
+struct RingTab;
+template <int GU = 8, class FT = double, int MODE = 0>
+__device__ __forceinline__ void push_one(const Geo& g, const RingTab* __restrict__ rt, double psi, double theta,
+                                         double zeta, double rho_par, double w, double mu, const double* base,
+                                         double h, const double* __restrict__ gf, double* X, long long& refl,
+                                         long long& clamps, double* gio = nullptr);
+__device__ __forceinline__ void load_ring_tab(const Geo& g, RingTab* rt);
+__device__ __forceinline__ void push_epilogue(DevCounters* dc, double wmax, long long refl, long long clamps,
+                                              int nonfinite);
+struct FusePush {
+    const double* src[5];
+    const double* base[5];
+    double* out[5];
+    const double* gf;
+    double h;
+    int s1;      // stage 1: the source is the base (read once)
+    int rt_off;  // byte offset of the push's ring table in dynamic shared memory
+};
+
+template <class R, int NB, bool FUSE = false>
 __global__ void __launch_bounds__(kDepositThreads, NB)
     k_deposit_tiled(Geo g, PSet s, long long n, const Tile* __restrict__ tiles, const int* ntiles_p,
-                    long long* __restrict__ fx, DevCounters* dc, int cap_nodes, double rho_cut) {
-    constexpr int kDepCap = deposit_cap_nodes(NB);
+                    long long* __restrict__ fx, DevCounters* dc, int cap_nodes, double rho_cut, FusePush fp = {}) {
+    constexpr int kDepCap = FUSE ? deposit_cap_nodes(3) : deposit_cap_nodes(NB);  // fused: the NB=3 window
     constexpr int kDepStride = kDepCap + 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     unsigned* slo = reinterpret_cast<unsigned*>(smem_raw);
@@ -388,6 +412,12 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
     const int lane = threadIdx.x & 31;
     const int b2 = (lane >> 2) & 1, b3 = (lane >> 3) & 1, b4 = (lane >> 4) & 1;
     if (threadIdx.x == 0) s_fallback = 0;
+    // fused push: its ring table, and its per-thread counters
+    const RingTab* prt = reinterpret_cast<const RingTab*>(smem_raw + fp.rt_off);
+    if constexpr (FUSE) load_ring_tab(g, reinterpret_cast<RingTab*>(smem_raw + fp.rt_off));
+    double p_wmax = 0.0;
+    long long p_refl = 0, p_clamps = 0;
+    int p_nonfinite = 0;
 
     for (;;) {
         if (threadIdx.x == 0) T.tile = atomicAdd(&dc->tile_next, 1);
@@ -496,16 +526,42 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
         const long long pend = T.end;
         long long p = T.start + threadIdx.x;
         double n_psi = 0.0, n_theta = 0.0, n_zeta = 0.0, n_w = 0.0, n_mu = 0.0;
-        if (p < pend) {
+        if (!FUSE && p < pend) {
             n_psi = ldp_cs<R>(s.x[0], p); n_theta = ldp_cs<R>(s.x[1], p); n_zeta = ldp_cs<R>(s.x[2], p);
             n_w = ldp_cs<R>(s.x[4], p); n_mu = ldp_cs<R>(s.mu, p);
         }
         for (; p < pend; p += blockDim.x) {
-            const double psi = n_psi, theta = n_theta, zeta = n_zeta, w = n_w, mu = n_mu;
-            const long long pn = p + blockDim.x;
-            if (pn < pend) {
-                n_psi = ldp_cs<R>(s.x[0], pn); n_theta = ldp_cs<R>(s.x[1], pn); n_zeta = ldp_cs<R>(s.x[2], pn);
-                n_w = ldp_cs<R>(s.x[4], pn); n_mu = ldp_cs<R>(s.mu, pn);
+            double psi, theta, zeta, w, mu;
+            if constexpr (FUSE) {
+                // push this marker (RK2 stage), store its new state, deposit it
+                double base[5], X[5];
+#pragma unroll
+                for (int d = 0; d < 5; d++) base[d] = ldp_cs<double>(fp.base[d], p);
+                mu = ldp_cs<double>(s.mu, p);
+                if (fp.s1) {
+                    push_one<8, double, 0>(g, prt, base[0], base[1], base[2], base[3], base[4], mu, base, fp.h, fp.gf,
+                                           X, p_refl, p_clamps, nullptr);
+                } else {
+                    push_one<8, double, 0>(g, prt, ldp_cs<double>(fp.src[0], p), ldp_cs<double>(fp.src[1], p),
+                                           ldp_cs<double>(fp.src[2], p), ldp_cs<double>(fp.src[3], p),
+                                           ldp_cs<double>(fp.src[4], p), mu, base, fp.h, fp.gf, X, p_refl, p_clamps,
+                                           nullptr);
+                }
+                if (!isfinite((X[0] + X[1] + X[2] + X[3]) * 0.0 + X[4])) p_nonfinite = 1;
+#pragma unroll
+                for (int d = 0; d < 5; d++) stp_cs<double>(fp.out[d], p, X[d]);
+                p_wmax = fmax(p_wmax, fabs(X[4]));
+                psi = X[0];
+                theta = X[1];
+                zeta = X[2];
+                w = X[4];
+            } else {
+                psi = n_psi; theta = n_theta; zeta = n_zeta; w = n_w; mu = n_mu;
+                const long long pn = p + blockDim.x;
+                if (pn < pend) {
+                    n_psi = ldp_cs<R>(s.x[0], pn); n_theta = ldp_cs<R>(s.x[1], pn); n_zeta = ldp_cs<R>(s.x[2], pn);
+                    n_w = ldp_cs<R>(s.x[4], pn); n_mu = ldp_cs<R>(s.mu, pn);
+                }
             }
             // a non-finite marker (flagged by the push) is never deposited
             if (!isfinite((psi + theta + zeta + mu) * 0.0 + w)) continue;
@@ -711,6 +767,7 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
         __syncthreads();
     }
     if (threadIdx.x == 0 && s_fallback) atomicAdd((unsigned long long*)&dc->fallback, s_fallback);
+    if constexpr (FUSE) push_epilogue(dc, p_wmax, p_refl, p_clamps, p_nonfinite);
 }
 
 // ---------------------------------------------------------------------------
@@ -948,6 +1005,51 @@ void launch_deposit_tiled(const Geo& g, const PSet& s, long long n, const Tile* 
     g_launches++;
 }
 
+// fused push + next-stage deposit: 2 CTAs/SM (the push's
+// 128 registers), the 3-CTA window capacity, the push's ring table behind the
+// deposit's shared memory
+size_t push_deposit_smem(const Geo& g, size_t* rt_off) {
+    const size_t off = (deposit_tiled_smem(g.P, 3) + 15) & ~(size_t)15;
+    if (rt_off) *rt_off = off;
+    return off + (size_t)(g.mpsi + 1) * 16;
+}
+
+int configure_push_deposit(const Geo& g) {
+    const size_t smem = push_deposit_smem(g, nullptr);
+    if (cudaFuncSetAttribute(k_deposit_tiled<double, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int r = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_deposit_tiled<double, 2, true>, kDepositThreads, smem) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return std::min(r, 2);
+}
+
+void launch_push_deposit(const Geo& g, const PSet& s, long long n, const Tile* tiles, long long* fx, DevCounters* dc,
+                         int ctas, int cap_nodes, const double* const src[5], const double* const base[5],
+                         double* const out[5], const double* gf, double h, cudaStream_t st) {
+    FusePush fp;
+    for (int d = 0; d < 5; d++) {
+        fp.src[d] = src[d];
+        fp.base[d] = base[d];
+        fp.out[d] = out[d];
+    }
+    fp.gf = gf;
+    fp.h = h;
+    fp.s1 = src[0] == base[0];
+    size_t off = 0;
+    const size_t smem = push_deposit_smem(g, &off);
+    fp.rt_off = (int)off;
+    k_deposit_tiled<double, 2, true><<<ctas, kDepositThreads, smem, st>>>(g, s, n, tiles, &dc->ntiles, fx, dc, cap_nodes,
+                                                                        deposit_rho_cut(g), fp);
+    g_launches++;
+}
+
 // fixed point -> fp64 on planes 0..planes-1 (canonical and duplicate nodes)
 __global__ void k_fx_to_real(Geo g, const long long* __restrict__ fx, double* __restrict__ rho,
                              const DevCounters* dc, int planes) {
@@ -1034,11 +1136,11 @@ __device__ __forceinline__ double warp_max(double v) {
 // MODE 0: fused gather + update (the product).  Loop-fission ablation of the
 // paper's Xeon Phi push: MODE 1 only gathers gbar into gio[0..2],
 // MODE 2 only updates from gio.
-template <int GU = 8, class FT = double, int MODE = 0>
+template <int GU, class FT, int MODE>
 __device__ __forceinline__ void push_one(const Geo& g, const RingTab* __restrict__ rt, double psi, double theta,
                                          double zeta, double rho_par, double w, double mu, const double* base,
                                          double h, const double* __restrict__ gf, double* X, long long& refl,
-                                         long long& clamps, double* gio = nullptr) {
+                                         long long& clamps, double* gio) {
     // U-1
     double st, ct;
     sincos_theta(theta, &st, &ct);

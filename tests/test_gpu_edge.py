@@ -285,3 +285,61 @@ def test_update_binning_charge_ablation_bitwise(G, orc, size, n):
         grids.append(ctx.get_grid(G.GRID_CHARGE))
         ctx.close()
     assert np.array_equal(grids[0], grids[1])
+
+
+def test_fused_stage_pipeline_step_parity_T(G, orc):
+    """SURVEY §8(f) #1 (gtcp_set_fused): the push of each RK2 stage deposits
+    the next stage's charge in the same kernel; one full step against the
+    oracle's step, three times along its trajectory (config T)."""
+    cfg = synth.config("T")
+    p = orc.make_params(cfg)
+    state = synth.load_particles(cfg, 12100, seed=51, w_amp=0.1)
+    nm = orc.marker_norm(p, state)
+    for _ in range(3):
+        ctx = ctx_for(G, "T")
+        ctx.set_fused(True)
+        ctx.set_particles(state)
+        ctx.set_grid(G.GRID_MARKER, nm)
+        ctx.step(1)
+        got = ctx.get_particles()
+        ctx.close()
+        ref = {k: v.copy() for k, v in state.items()}
+        orc.step_global(p, ref, nm)
+        assert_particles_close(got, ref)
+        state = ref
+
+
+def test_fused_stage_pipeline_matches_unfused_A(G):
+    """Class-A grid, 2 M markers, 3 steps in one gtcp_step call: the fused
+    pipeline (5 of the 6 charges deposited inside the preceding push) gives the
+    unfused trajectory within the fixed-point rounding of the charge (its
+    scale has one bit of headroom), and its charge phase really shrank."""
+    cfg = synth.config("A")
+    parts = synth.load_particles(cfg, 2_000_000, seed=52, w_amp=0.1)
+    outs, charge_ms = [], []
+    for fused in (False, True):
+        ctx = ctx_for(G, "A")
+        ctx.set_fused(fused)
+        ctx.set_particles(parts)
+        ctx.set_timing(True)
+        ctx.timings_reset()
+        ctx.step(3)
+        charge_ms.append(ctx.timings()["charge_ms"])
+        outs.append(ctx.get_particles())
+        ctx.close()
+    o0, o1 = np.argsort(outs[0]["id"]), np.argsort(outs[1]["id"])
+    assert np.array_equal(outs[0]["id"][o0], outs[1]["id"][o1])
+    for k in ("psi", "rho", "w"):
+        assert rel_err(outs[1][k][o1], outs[0][k][o0]) <= 1e-9, k
+    for k in ("theta", "zeta"):
+        d = (outs[1][k][o1] - outs[0][k][o0] + math.pi) % TWO_PI - math.pi
+        assert np.max(np.abs(d)) <= 1e-9, k
+    assert charge_ms[1] < 0.5 * charge_ms[0], charge_ms
+
+
+def test_fused_stage_pipeline_rejects_unsupported(G):
+    ctx = G.Context(G.gtcp_default_params("T", precision=32))
+    with pytest.raises(Exception):
+        ctx.set_fused(True)
+    ctx.set_fused(False)
+    ctx.close()

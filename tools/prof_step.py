@@ -20,6 +20,7 @@ ap.add_argument("--bin-mu", type=int, default=None)
 ap.add_argument("--mzetamax", type=int, default=None)
 ap.add_argument("--precision", type=int, default=64)
 ap.add_argument("--field-f32", type=int, default=0)
+ap.add_argument("--fused", type=int, default=0)
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -37,6 +38,8 @@ over["field_f32"] = a.field_f32
 stream = torch.cuda.Stream()
 ctx = G.Context(G.gtcp_default_params(a.size, bin_every=a.bin_every, **over), stream=stream.cuda_stream)
 ctx.set_charge_mode(a.charge_mode)
+if a.fused:
+    ctx.set_fused(True)
 ctx.load()
 ctx.step(a.warmup)
 ctx.set_timing(True)
