@@ -392,6 +392,12 @@ struct FusePush {
     int rt_off;  // byte offset of the push's ring table in dynamic shared memory
 };
 
+#ifndef GTCP_FUSED_NB  // experiment builds: CTAs per SM / gather unroll of the fused push + deposit
+#define GTCP_FUSED_NB 2
+#endif
+#ifndef GTCP_FUSED_GU
+#define GTCP_FUSED_GU 8
+#endif
 template <class R, int NB, bool FUSE = false>
 __global__ void __launch_bounds__(kDepositThreads, NB)
     k_deposit_tiled(Geo g, PSet s, long long n, const Tile* __restrict__ tiles, const int* ntiles_p,
@@ -539,10 +545,10 @@ __global__ void __launch_bounds__(kDepositThreads, NB)
                 for (int d = 0; d < 5; d++) base[d] = ldp_cs<double>(fp.base[d], p);
                 mu = ldp_cs<double>(s.mu, p);
                 if (fp.s1) {
-                    push_one<8, double, 0>(g, prt, base[0], base[1], base[2], base[3], base[4], mu, base, fp.h, fp.gf,
-                                           X, p_refl, p_clamps, nullptr);
+                    push_one<GTCP_FUSED_GU, double, 0>(g, prt, base[0], base[1], base[2], base[3], base[4], mu, base,
+                                                       fp.h, fp.gf, X, p_refl, p_clamps, nullptr);
                 } else {
-                    push_one<8, double, 0>(g, prt, ldp_cs<double>(fp.src[0], p), ldp_cs<double>(fp.src[1], p),
+                    push_one<GTCP_FUSED_GU, double, 0>(g, prt, ldp_cs<double>(fp.src[0], p), ldp_cs<double>(fp.src[1], p),
                                            ldp_cs<double>(fp.src[2], p), ldp_cs<double>(fp.src[3], p),
                                            ldp_cs<double>(fp.src[4], p), mu, base, fp.h, fp.gf, X, p_refl, p_clamps,
                                            nullptr);
@@ -1016,18 +1022,18 @@ size_t push_deposit_smem(const Geo& g, size_t* rt_off) {
 
 int configure_push_deposit(const Geo& g) {
     const size_t smem = push_deposit_smem(g, nullptr);
-    if (cudaFuncSetAttribute(k_deposit_tiled<double, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(k_deposit_tiled<double, GTCP_FUSED_NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
     int r = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_deposit_tiled<double, 2, true>, kDepositThreads, smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_deposit_tiled<double, GTCP_FUSED_NB, true>, kDepositThreads, smem) !=
         cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
-    return std::min(r, 2);
+    return std::min(r, GTCP_FUSED_NB);
 }
 
 void launch_push_deposit(const Geo& g, const PSet& s, long long n, const Tile* tiles, long long* fx, DevCounters* dc,
@@ -1045,7 +1051,7 @@ void launch_push_deposit(const Geo& g, const PSet& s, long long n, const Tile* t
     size_t off = 0;
     const size_t smem = push_deposit_smem(g, &off);
     fp.rt_off = (int)off;
-    k_deposit_tiled<double, 2, true><<<ctas, kDepositThreads, smem, st>>>(g, s, n, tiles, &dc->ntiles, fx, dc, cap_nodes,
+    k_deposit_tiled<double, GTCP_FUSED_NB, true><<<ctas, kDepositThreads, smem, st>>>(g, s, n, tiles, &dc->ntiles, fx, dc, cap_nodes,
                                                                         deposit_rho_cut(g), fp);
     g_launches++;
 }
