@@ -310,10 +310,12 @@ def test_fused_stage_pipeline_step_parity_T(G, orc):
 
 
 def test_fused_stage_pipeline_matches_unfused_A(G):
-    """Class-A grid, 2 M markers, 3 steps in one gtcp_step call: the fused
-    pipeline (5 of the 6 charges deposited inside the preceding push) gives the
-    unfused trajectory within the fixed-point rounding of the charge (its
-    scale has one bit of headroom), and its charge phase really shrank."""
+    """Class-A grid, 2 M markers, 4 steps in two gtcp_step calls (a bin after
+    step 3; the charge deposited by the last push of the first call is used by
+    the second): the fused pipeline (7 of the 8 charges deposited inside the
+    preceding push) gives the unfused trajectory within the fixed-point
+    rounding of the charge (its scale has one bit of headroom), and its charge
+    phase really shrank."""
     cfg = synth.config("A")
     parts = synth.load_particles(cfg, 2_000_000, seed=52, w_amp=0.1)
     outs, charge_ms = [], []
@@ -323,7 +325,8 @@ def test_fused_stage_pipeline_matches_unfused_A(G):
         ctx.set_particles(parts)
         ctx.set_timing(True)
         ctx.timings_reset()
-        ctx.step(3)
+        ctx.step(2)
+        ctx.step(2)
         charge_ms.append(ctx.timings()["charge_ms"])
         outs.append(ctx.get_particles())
         ctx.close()
