@@ -247,8 +247,8 @@ void orc_charge_reduce_global(const orc_params* p, double* grid) {
 
 /* Q-8 (reading; paper silent): marker density per ring = flux-surface mean
  * (over planes 0..mzetamax-1 and canonical nodes) of the reduced charge
- * deposited with w = 1.  Parity unpinned beyond conservation (its input is
- * the pinned deposit). */
+ * deposited with w = 1.  Pinned by conservation and by the closed form of
+ * markers sitting on nodes with mu = 0 (tests/test_oracle_charge.py). */
 void orc_marker_norm(const orc_params* p, int64_t n, const double* psi, const double* theta,
                      const double* zeta, const double* mu, double* nm) {
     orc_geom g;

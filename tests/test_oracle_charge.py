@@ -186,3 +186,32 @@ def test_gather_mu0_at_node(orc, T):
     theta = j * TWO_PI / g.mtheta[i]
     gb = orc.gather(p, _one(0.5 * r * r, theta, zeta, 0.0), f)
     assert np.max(np.abs(gb[0] - f[0, g.igrid[i] + j])) < 1e-9
+
+
+def test_marker_norm_node_markers_closed_form(orc, T):
+    """Q-8 pinned by hand: markers with mu = 0 (the four gyro-points coincide)
+    sitting on grid nodes (r = r_i, zeta on a plane, theta on a field-line
+    label) each deposit exactly one unit on their own ring, so the marker
+    density of ring i is (markers on ring i) / (mzetamax * mtheta_i): the mean
+    over the mzetamax planes and the mtheta_i canonical nodes (not mtheta_i + 1
+    with the duplicate, nor mzetamax + 1 planes with the seam copy)."""
+    cfg, p, g = T
+    rng = np.random.default_rng(12)
+    K, M = p.mzetamax, p.mpsi
+    dr = (p.a1 - p.a0) / M
+    cnt = np.zeros(M + 1)
+    psi, theta, zeta = [], [], []
+    for i in range(M + 1):
+        for _ in range(i % 5 + 1):
+            k = int(rng.integers(K))
+            j = int(rng.integers(g.mtheta[i]))
+            z = k * 2 * math.pi / K
+            r = p.a0 + i * dr
+            psi.append(0.5 * r * r)
+            zeta.append(z)
+            theta.append((2 * math.pi * j / g.mtheta[i] + z * g.qtinv[i]) % (2 * math.pi))
+            cnt[i] += 1
+    parts = dict(psi=np.array(psi), theta=np.array(theta), zeta=np.array(zeta), mu=np.zeros(len(psi)))
+    nm = orc.marker_norm(p, parts)
+    expect = cnt / (K * np.asarray(g.mtheta[:M + 1], dtype=float))
+    assert np.allclose(nm, expect, rtol=0, atol=1e-12 * expect.max())

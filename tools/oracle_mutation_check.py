@@ -57,6 +57,11 @@ MUTATIONS = [
     ("push: kappa without the energy dependence",
      "double kappa = orc_prof(r) * (p->rln + (Ekin - 1.5) * p->rlt) / p->R0;",
      "double kappa = orc_prof(r) * (p->rln + p->rlt) / p->R0;"),
+    ("marker density: divided by mtheta + 1 (duplicate node counted)",
+     "nm[i] = s / ((double)p->mzetamax * g.mtheta[i]);", "nm[i] = s / ((double)p->mzetamax * (g.mtheta[i] + 1));"),
+    ("marker density: seam plane included in the mean",
+     "        for (int32_t k = 0; k < p->mzetamax; k++)\n            for (int32_t j = 0; j < g.mtheta[i]; j++)\n                s += grid",
+     "        for (int32_t k = 0; k <= p->mzetamax; k++)\n            for (int32_t j = 0; j < g.mtheta[i]; j++)\n                s += grid"),
     ("field g_r neighbour rings at the same label (not physical theta)",
      "gr = (ring_interp(p, &g, pl, i + 1, th, zeta_k) -\n                          ring_interp(p, &g, pl, i - 1, th, zeta_k)) / (2.0 * dr);",
      "gr = (ring_interp(p, &g, pl, i + 1, j * TWO_PI / g.mtheta[i + 1], 0.0) -\n"
