@@ -1381,7 +1381,11 @@ void launch_push3(const Geo& g, const double* const src[5], const double* const 
     // one particle per thread, 2 CTAs of 256 per SM (128 registers); measured
     // alternatives (3 CTAs, 96-register shapes, TMA- or smem-staged streams and
     // field windows, a texture-path gather) were all slower
-    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
+    // exactly the resident CTAs (2 per SM), each striding over the particles:
+    // no partial last wave (measured 148 x 2 / 4 / 8 / 16 / 32 CTAs at A:
+    // 19.58 / 19.58 / 19.97 / 20.47 / 20.75 ms/step)
+    static const int pgm = getenv("GTCP_PUSH_GRID") ? atoi(getenv("GTCP_PUSH_GRID")) : 2;  // experiments
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * pgm);
     size_t smr = (g.mpsi + 1) * sizeof(RingTab);
     if (g3 && !g.prec32 && !g.f32field) {
         // loop-fission ablation: gather loop, then update loop
