@@ -909,11 +909,15 @@ static void push_range(gtcp_ctx c, double* const* src, double* const* base, doub
     const bool fuse = c->prm.ntoroidal > 1 && c->cls != nullptr;
     unsigned* cntL = c->bcount;
     unsigned* cntR = cntL + (c->shift_blocks + 1);
-    if (fuse) CU_VOID(cudaMemsetAsync(cntL, 0, 2 * (c->shift_blocks + 1) * sizeof(unsigned), c->st));
+    if (fuse) {
+        CU_VOID(cudaMemsetAsync(cntL, 0, 2 * (c->shift_blocks + 1) * sizeof(unsigned), c->st));
+        CU_VOID(cudaMemsetAsync(c->d_counts + 5, 0, sizeof(long long), c->st));  // multi-hop flag
+    }
     c->cls_ready = fuse;
     if (c->n > 0)
         launch_push3(c->geo, src, base, out, c->mu, c->n, h, c->gfield, c->dc, c->st, fuse ? c->cls : nullptr,
-                     fuse ? cntL : nullptr, fuse ? cntR : nullptr, c->push_mode == 1 ? c->g3 : nullptr);
+                     fuse ? cntL : nullptr, fuse ? cntR : nullptr, c->push_mode == 1 ? c->g3 : nullptr,
+                     fuse ? c->d_counts + 5 : nullptr);
 }
 
 static gtcp_status push_impl(gtcp_ctx c, int stage);
@@ -1541,9 +1545,10 @@ gtcp_status shift_exchange(gtcp_ctx c, int dir) {
         unsigned* offH = offR + (c->shift_blocks + 1);
         unsigned* offF = offH + (c->shift_blocks + 1);
         if (dir == 0 && iter == 0 && c->cls_ready) {
-            // classification and per-chunk counts came fused out of the push
+            // classification, per-chunk counts and the multi-hop flag came fused out of the push
         } else {
-            launch_shift_classify(g, attrs[2], attrs[0], dir, n, c->cls, cntL, cntR, c->st);
+            CU(cudaMemsetAsync(c->d_counts + 5, 0, sizeof(long long), c->st));
+            launch_shift_classify(g, attrs[2], attrs[0], dir, n, c->cls, cntL, cntR, c->d_counts + 5, c->st);
         }
         if (dir == 0) c->cls_ready = false;
         launch_scan_u32(cntL, offL, nb, c->scan_tmp, c->st);
@@ -1559,12 +1564,14 @@ gtcp_status shift_exchange(gtcp_ctx c, int dir) {
         if (left >= 0) NC(comm_recv(comm, c->d_counts + 3, 1, ncclInt64, left, c->st, acct));    // left's right-movers
         NC(comm_group_end());
         launch_sum_i64_pair(c->d_counts, c->d_counts + 4, c->st);
-        NC(comm_allreduce(comm, c->d_counts + 4, c->d_counts + 5, 1, ncclInt64, ncclSum, c->st, acct));
-        CU(cudaMemcpyAsync(c->h_counts, c->d_counts, 6 * sizeof(long long), cudaMemcpyDeviceToHost, c->st));
+        // [mine, multi-hop flag] summed over the ring / line -> [total, any multi-hop]
+        NC(comm_allreduce(comm, c->d_counts + 4, c->d_counts + 6, 2, ncclInt64, ncclSum, c->st, acct));
+        CU(cudaMemcpyAsync(c->h_counts, c->d_counts, 8 * sizeof(long long), cudaMemcpyDeviceToHost, c->st));
         if (iter == 0) mark();
         CU(cudaStreamSynchronize(c->st));
         const long long nL = c->h_counts[0], nR = c->h_counts[1], rR = c->h_counts[2], rL = c->h_counts[3];
-        const long long total = c->h_counts[5];
+        const long long total = c->h_counts[6];
+        const bool multi_hop = c->h_counts[7] != 0;
         if (total == 0) {
             settled = true;
             break;
@@ -1610,6 +1617,12 @@ gtcp_status shift_exchange(gtcp_ctx c, int dir) {
         c->movers_recv += rL + rR;
         c->n = start + nkeep + rL + rR;
         start = start + nkeep;  // only the arrivals can still be misplaced
+        // no mover went beyond a neighbouring domain anywhere on the ring /
+        // line: every arrival is home, the re-check pass would find none
+        if (!multi_hop) {
+            settled = true;
+            break;
+        }
     }
     if (!settled) return set_err(c, GTCP_EINVARIANT, "shift: movers left after the multi-hop guard");
     // (the fixed-point charge scale needs max|w| of the new particle set: the

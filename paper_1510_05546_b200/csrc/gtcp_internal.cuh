@@ -119,7 +119,7 @@ void launch_fx_to_real(const Geo& g, const long long* fx, double* rho, const Dev
 void launch_push3(const Geo& g, const double* const src[5], const double* const base[5], double* const out[5],
                   const double* mu, long long n, double h, const double* gfield, DevCounters* dc, cudaStream_t st,
                   unsigned char* cls = nullptr, unsigned* cntL = nullptr, unsigned* cntR = nullptr,
-                  double* g3 = nullptr);  // g3 != null: loop-fission ablation (3 n doubles of gbar)
+                  double* g3 = nullptr, long long* far = nullptr);  // g3 != null: loop-fission ablation (3 n doubles of gbar)
 void launch_wmax(const double* w, long long n, DevCounters* dc, cudaStream_t st);
 void launch_bin_keys(const Geo& g, const PSet& s, long long n, unsigned* key, unsigned* rank, unsigned* count,
                      cudaStream_t st);
@@ -171,7 +171,7 @@ void launch_field_energy(const Geo& g, const double* phi, double* out, double* p
 // shift (gtcp_shift.cu)
 int shift_chunks(long long n);
 void launch_shift_classify(const Geo& g, const double* zeta, const double* psi, int mode, long long n,
-                           unsigned char* cls, unsigned* cntL, unsigned* cntR, cudaStream_t st);
+                           unsigned char* cls, unsigned* cntL, unsigned* cntR, long long* far, cudaStream_t st);
 void launch_shift_nkeep(long long n, const unsigned* totL, const unsigned* totR, long long* nkeep, long long* counts,
                         cudaStream_t st);
 void launch_shift_count_holes(const unsigned char* cls, long long n, const long long* nkeep, unsigned* cntH,

@@ -1108,6 +1108,7 @@ struct PushPtrs {
     unsigned char* cls;
     unsigned* cntL;
     unsigned* cntR;
+    long long* far;  // set to 1 if any particle moves beyond a neighbouring domain
 };
 
 #ifndef GTCP_PUSH_MINB  // experiment builds: CTAs per SM / gather unroll of the fp64 push
@@ -1120,11 +1121,13 @@ static constexpr int kShiftChunkLog2 = 14;  // == log2(kChunk) of gtcp_shift.cu
 
 // same expression as the shift's classify (mode 0): destination toroidal domain
 // floor(kg / P) of the new zeta, the shorter way round the torus
-__device__ __forceinline__ unsigned char toroidal_class(const Geo& g, double zeta) {
+// far: the destination is beyond the neighbouring domain (a multi-hop mover)
+__device__ __forceinline__ unsigned char toroidal_class(const Geo& g, double zeta, bool* far) {
     double wz1;
     const int d = plane_of(g, zeta, &wz1) / g.P;
     int rel = d - g.rank_t;
     if (rel < 0) rel += g.ntor;
+    *far = rel > 1 && rel < g.ntor - 1;
     if (rel == 0) return 0;
     return (rel <= g.ntor / 2) ? 2 : 1;
 }
@@ -1349,8 +1352,10 @@ __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long lon
         }
         if (pp.cls) {
             // classify on the value as stored (fp32 state rounds zeta)
-            const unsigned char c = toroidal_class(g, (double)(R)X[2]);
+            bool far;
+            const unsigned char c = toroidal_class(g, (double)(R)X[2], &far);
             pp.cls[p] = c;
+            if (far) *pp.far = 1;
             // the 32 lanes of a warp hold consecutive p inside one chunk
             const unsigned act = __activemask();
             const unsigned bl = __ballot_sync(act, c == 1), br = __ballot_sync(act, c == 2);
@@ -1366,7 +1371,7 @@ __global__ void __launch_bounds__(256, MINB) k_push(Geo g, PushPtrs pp, long lon
 
 void launch_push3(const Geo& g, const double* const src[5], const double* const base[5], double* const out[5],
                   const double* mu, long long n, double h, const double* gfield, DevCounters* dc,
-                  cudaStream_t st, unsigned char* cls, unsigned* cntL, unsigned* cntR, double* g3) {
+                  cudaStream_t st, unsigned char* cls, unsigned* cntL, unsigned* cntR, double* g3, long long* far) {
     if (n <= 0) return;
     PushPtrs pp;
     for (int d = 0; d < 5; d++) {
@@ -1378,6 +1383,7 @@ void launch_push3(const Geo& g, const double* const src[5], const double* const 
     pp.cls = cls;
     pp.cntL = cntL;
     pp.cntR = cntR;
+    pp.far = far;
     // one particle per thread, 2 CTAs of 256 per SM (128 registers); measured
     // alternatives (3 CTAs, 96-register shapes, TMA- or smem-staged streams and
     // field windows, a texture-path gather) were all slower

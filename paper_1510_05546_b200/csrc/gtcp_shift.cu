@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kLT) k_shift_classify(Geo g, const double* __r
                                                         const double* __restrict__ psi, int mode, long long n,
                                                         unsigned char* __restrict__ cls,
                                                         unsigned* __restrict__ cntL,
-                                                        unsigned* __restrict__ cntR) {
+                                                        unsigned* __restrict__ cntR, long long* far) {
     __shared__ unsigned sw[33];
     const long long base = (long long)blockIdx.x * kChunk;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -174,9 +174,11 @@ __global__ void __launch_bounds__(kLT) k_shift_classify(Geo g, const double* __r
                     int rel = d - g.rank_t;
                     if (rel < 0) rel += g.ntor;
                     if (rel != 0) c = (rel <= g.ntor / 2) ? 2 : 1;
+                    if (rel > 1 && rel < g.ntor - 1) *far = 1;  // beyond a neighbour: multi-hop
                 } else {
                     int rel = radial_domain(g, z[j]) - g.rank_r;
                     if (rel != 0) c = (rel > 0) ? 2 : 1;
+                    if (rel > 1 || rel < -1) *far = 1;
                 }
                 cls[p] = c;
             }
@@ -317,10 +319,10 @@ int shift_chunks(long long n) { return (int)std::max<long long>(1, (n + kChunk -
 
 // ---------------------------------------------------------------------------
 void launch_shift_classify(const Geo& g, const double* zeta, const double* psi, int mode, long long n,
-                           unsigned char* cls, unsigned* cntL, unsigned* cntR, cudaStream_t st) {
+                           unsigned char* cls, unsigned* cntL, unsigned* cntR, long long* far, cudaStream_t st) {
     int nb = shift_chunks(n);
-    if (g.prec32) k_shift_classify<float><<<nb, kLT, 0, st>>>(g, zeta, psi, mode, n, cls, cntL, cntR);
-    else k_shift_classify<double><<<nb, kLT, 0, st>>>(g, zeta, psi, mode, n, cls, cntL, cntR);
+    if (g.prec32) k_shift_classify<float><<<nb, kLT, 0, st>>>(g, zeta, psi, mode, n, cls, cntL, cntR, far);
+    else k_shift_classify<double><<<nb, kLT, 0, st>>>(g, zeta, psi, mode, n, cls, cntL, cntR, far);
     g_launches++;
 }
 

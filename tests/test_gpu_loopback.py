@@ -112,3 +112,33 @@ def test_loopback_comm_bytes_counted(H):
         assert tm["charge_red_comm_bytes"] >= 2 * 8 * mgrid  # one int64 ghost plane per stage, at least
         assert tm["shift_comm_bytes"] >= 6 * 8 * st["movers_sent"]
         assert tm["poisson_comm_bytes"] > 0
+
+
+def test_loopback_multi_hop_shift(H):
+    """Multi-hop shift: 4 toroidal domains, each rank handed the
+    particles of the domain two hops away; one gtcp_shift must deliver every
+    particle to its owner (the movers' multi-hop flag forces the re-check
+    passes that a one-hop shift skips), conserving the count and the ids."""
+    import paper_1510_05546_b200 as G
+    import synth
+    P, K = 2, 8
+    ranks = H.LoopbackRanks(H.layout_params("T", 4, mzetamax=K))
+    try:
+        cfg = synth.config("T", mzetamax=K)
+        parts = synth.load_particles(cfg, 12000, seed=9)
+        kg = np.minimum(np.floor(parts["zeta"] * K / (2 * math.pi)).astype(int), K - 1)
+        owner = kg // P
+
+        def go(r):
+            c = ranks.ctx[r]
+            c.set_particles({k: v[owner == (r + 2) % 4] for k, v in parts.items()})
+            c.shift()
+            got = c.get_particles()
+            kk = np.minimum(np.floor(got["zeta"] * K / (2 * math.pi)).astype(int), K - 1)
+            return got["id"], bool(np.all(kk // P == r))
+        res = ranks.each(go)
+    finally:
+        ranks.close()
+    assert all(ok for _, ok in res)
+    ids = np.sort(np.concatenate([i for i, _ in res]))
+    assert np.array_equal(ids, np.sort(parts["id"]))

@@ -53,7 +53,7 @@ int main(int argc, char** argv) {
     unsigned *fills, *midx;
     cudaMalloc(&fills, cap * sizeof(unsigned));
     cudaMalloc(&midx, 2 * cap * sizeof(unsigned));
-    long long *nkeep, *counts; cudaMalloc(&nkeep, 8); cudaMalloc(&counts, 64);
+    long long *nkeep, *counts, *far_flag; cudaMalloc(&nkeep, 8); cudaMalloc(&counts, 64); cudaMalloc(&far_flag, 8);
     unsigned *cL = cnt, *cR = cL + nb + 1, *cH = cR + nb + 1, *cF = cH + nb + 1, *oL = cF + nb + 1, *oR = oL + nb + 1,
              *oH = oR + nb + 1, *oF = oH + nb + 1;
     cudaEvent_t e[8];
@@ -61,7 +61,7 @@ int main(int argc, char** argv) {
     for (int r = 0; r < reps; r++) {
         init_zeta<<<148 * 16, 256>>>(a[2], n, frac, 32 * g.dzeta, 7 + r);
         cudaEventRecord(e[0]);
-        launch_shift_classify(g, a[2], a[2], mode, n, cls, cL, cR, 0);
+        launch_shift_classify(g, a[2], a[2], mode, n, cls, cL, cR, far_flag, 0);
         launch_scan_u32(cL, oL, nb, scan_tmp, 0);
         launch_scan_u32(cR, oR, nb, scan_tmp, 0);
         launch_shift_nkeep(n, oL + nb, oR + nb, nkeep, counts, 0);
