@@ -1473,7 +1473,10 @@ __global__ void k_bin_keys(Geo g, PSet s, long long n, unsigned* __restrict__ ke
 void launch_bin_keys(const Geo& g, const PSet& s, long long n, unsigned* key, unsigned* rank, unsigned* count,
                      cudaStream_t st) {
     if (n <= 0) return;
-    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    // measured at A (ms per bin) for 148 x {4, 8, 16, 32, 64, 128} CTAs: 2.37 /
+    // 2.40 / 1.95 / 1.94 / 1.84 / 1.84
+    static const int gm = getenv("GTCP_KEYS_GRID") ? atoi(getenv("GTCP_KEYS_GRID")) : 64;  // experiments
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * gm);
     if (g.prec32) k_bin_keys<float><<<blocks, 256, 0, st>>>(g, s, n, key, rank, count);
     else k_bin_keys<double><<<blocks, 256, 0, st>>>(g, s, n, key, rank, count);
     g_launches++;
@@ -1574,7 +1577,11 @@ __global__ void k_bin_inverse(const unsigned* __restrict__ key, const unsigned* 
 void launch_bin_inverse(const unsigned* key, const unsigned* rank, const unsigned* offset, long long n,
                         unsigned* inv, cudaStream_t st) {
     if (n <= 0) return;
-    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    // measured at A (ms per bin) for 148 x {1, 2, 3, 4, 6, 8, 16, 64} CTAs:
+    // 1.58 / 0.91 / 0.71 / 0.68 / 1.17 / 1.35 / 1.30 / 1.20 (the scattered
+    // 4-byte writes of the inverse merge best with 4 resident CTAs per SM)
+    static const int gm = getenv("GTCP_INV_GRID") ? atoi(getenv("GTCP_INV_GRID")) : 4;  // experiments
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * gm);
     k_bin_inverse<<<blocks, 256, 0, st>>>(key, rank, offset, n, inv);
     g_launches++;
 }
