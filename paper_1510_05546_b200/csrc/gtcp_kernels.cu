@@ -1633,7 +1633,11 @@ void launch_gather_perm_multi(const double* const* src, double* const* dst, int 
     A.na = na;
     A.id_src = id_src;
     A.id_dst = id_dst;
-    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    // measured (ms per bin) for 148 x {2, 3, 4, 5, 6, 7, 8, 10, 12, 16, 24} CTAs:
+    // class A 10.5 / 7.6 / 6.2 / 5.4 / 4.9 / 7.1 / 6.4 / 5.5 / 5.4 / 5.4 / 5.3;
+    // the class-B grid at 241 M markers: x6 5.7, x16 6.2
+    static const int gm = getenv("GTCP_PERM_GRID") ? atoi(getenv("GTCP_PERM_GRID")) : 6;  // experiments
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * gm);
     if (g_prec32) k_gather_perm_multi<float><<<blocks, 256, 0, st>>>(A, inv, n);
     else k_gather_perm_multi<double><<<blocks, 256, 0, st>>>(A, inv, n);
     g_launches++;
