@@ -175,9 +175,11 @@ __global__ void k_ring_sum(Geo g, const double* __restrict__ fH, double* __restr
     int i = blockIdx.x;
     int mt = __ldg(g.mtheta + i), ig = __ldg(g.igrid + i);
     double s = 0.0;
-    for (int e = threadIdx.x; e < g.P * mt; e += blockDim.x) {
-        int k = e / mt, j = e - k * mt;
-        s += fH[(long long)(k + 1) * g.mgrid + ig + j];
+    // plane by plane (no index division; consecutive threads read consecutive
+    // labels), a fixed summation order: deterministic
+    for (int k = 0; k < g.P; k++) {
+        const double* row = fH + (long long)(k + 1) * g.mgrid + ig;
+        for (int j = threadIdx.x; j < mt; j += blockDim.x) s += row[j];
     }
     __shared__ double sm[32];
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -191,14 +193,14 @@ __global__ void k_ring_sum(Geo g, const double* __restrict__ fH, double* __restr
 }
 
 void launch_ring_sum(const Geo& g, const double* f, double* ringsum, cudaStream_t st) {
-    k_ring_sum<<<g.mpsi + 1, 256, 0, st>>>(g, f, ringsum);
+    k_ring_sum<<<g.mpsi + 1, 1024, 0, st>>>(g, f, ringsum);
     g_launches++;
 }
 
 // ring sums of a plain (non-halo) plane-major array over planes 0..P-1
 void launch_marker_from_rho(const Geo& g, const double* rho, double* ringsum, cudaStream_t st) {
     // rho has planes 0..P at offset k*mgrid: view it as an H array shifted by one plane
-    k_ring_sum<<<g.mpsi + 1, 256, 0, st>>>(g, rho - g.mgrid, ringsum);
+    k_ring_sum<<<g.mpsi + 1, 1024, 0, st>>>(g, rho - g.mgrid, ringsum);
     g_launches++;
 }
 
