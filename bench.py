@@ -407,6 +407,10 @@ def run_gpu(args):
         }
         if world > 1:
             out["comm"] = comm
+        variant = [f"charge_mode {args.charge_mode}"] * bool(args.charge_mode) + \
+                  [f"push_mode {args.push_mode}"] * bool(args.push_mode) + ["fused stage pipeline"] * bool(args.fused)
+        if variant:  # ablation / option lines say so
+            out["config"]["variant"] = ", ".join(variant)
         print(json.dumps(out), flush=True)
     ctx.close()
     if dist:
