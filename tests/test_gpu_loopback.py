@@ -6,7 +6,8 @@ plane-split Poisson broadcasts, shift counts and payload -- with
 one cudaMemcpyAsync per message.  The library code path above the transport
 is the one NCCL runs (tests/dist_parity.py).  Layouts: toroidal 2 and 4,
 particle replicas 2, radial windows 2 (fp32 state) and 4, toroidal x radial
-2 x 2 and 2 x 4 (8 ranks), at T and at class-A geometry with 0.4-1 M markers;
+2 x 2 and 2 x 4 (8 ranks), at T and at class-A geometry with 0.4-1 M markers,
+class B as 8 toroidal domains of 8 planes (the 8-GPU bench layout);
 plus the fixed-point scale
 agreement regressions (replicas / toroidal ranks whose max|w| fall in
 different binades)."""
@@ -50,6 +51,7 @@ CASES = [
     dict(size="A", world=4, nparts=1_000_000, steps=1),
     dict(size="A", world=2, npartdom=2, nparts=1_000_000, steps=1),
     dict(size="A", world=2, nradial=2, precision=32, nparts=1_000_000, steps=1),
+    dict(size="B", world=8, nparts=1_000_000, steps=1),  # the N = 8 bench layout: 8 toroidal x 8 planes
 ]
 
 
