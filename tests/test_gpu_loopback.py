@@ -144,3 +144,16 @@ def test_loopback_multi_hop_shift(H):
     assert all(ok for _, ok in res)
     ids = np.sort(np.concatenate([i for i, _ in res]))
     assert np.array_equal(ids, np.sort(parts["id"]))
+
+
+def test_loopback_fused_pipeline_is_one_rank_only(H):
+    """gtcp_set_fused is a one-rank option: a decomposed
+    context rejects it (GTCP_EINVAL) and keeps stepping unfused."""
+    ranks = H.LoopbackRanks(H.layout_params("T", 2, mzetamax=8))
+    try:
+        for c in ranks.ctx:
+            with pytest.raises(Exception):
+                c.set_fused(True)
+            c.set_fused(False)
+    finally:
+        ranks.close()
