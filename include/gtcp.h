@@ -223,7 +223,25 @@ gtcp_status gtcp_sample_particles(gtcp_ctx ctx, int64_t m, const int64_t* idx, d
  * (Q-7): duplicate fold, ghost-plane merge with the right neighbour (seam
  * rotation at zeta = 2 pi), particle-replica allreduce. */
 gtcp_status gtcp_charge(gtcp_ctx ctx);
+/* Gyrokinetic Poisson equation and smoothing (§2 Eq. 14
+ * and P:221 §3.1; readings F-1..F-4): the charge of the last
+ * gtcp_charge (or gtcp_set_grid CHARGE) normalised by the marker density
+ * (Q-8) and smoothed (F-4); the flux-surface mean removed; poisson_iters
+ * weighted-Jacobi sweeps of (1 + 1/tau) phi - G(G(phi)) = dn with G the
+ * 4-point gyro-average (F-1, F-2); the zonal component added from its 1-D
+ * radial solve (F-3); phi smoothed again (F-4).  Result: the potential of
+ * the local planes with their halo planes (gtcp_get_grid PHI), consumed by
+ * gtcp_field.  Collectives: ring sums over the toroidal ring, the plane
+ * split of the sweeps over a section's ranks, halo exchanges.  Errors:
+ * GTCP_ECUDA, GTCP_ENCCL. */
 gtcp_status gtcp_poisson_smooth(gtcp_ctx ctx);
+/* Field (§3.1, reading F-5): the gradient triplet (g_r = dphi/dr at
+ * the node's physical angle, g_theta = dphi/dtheta, g_par = dphi/dzeta at
+ * fixed field-line label, centred differences) of the current phi on planes
+ * 0..P of this rank,
+ * written into the push's gather layout (interval-interleaved records,
+ * DESIGN.md §5; gtcp_get_grid GRADPHI returns it plane-major).  Errors:
+ * GTCP_ECUDA. */
 gtcp_status gtcp_field(gtcp_ctx ctx);
 /* stage 1: X0 <- X, X <- X + dt/2 F(X);  stage 2: X <- X0 + dt F(X) (U-7).
  * ESTATE if stage is not the one expected. */
