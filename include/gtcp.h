@@ -192,8 +192,13 @@ gtcp_status gtcp_nccl_unique_id(void* out128);
  * EINVARIANT if mzetamax % ntoroidal != 0 or the product != nranks. */
 gtcp_status gtcp_init(const gtcp_params* p, int rank, int nranks, const void* nccl_id,
                       void* cuda_stream, gtcp_ctx* out);
+/* Free the context and everything it allocated (device memory, pinned
+ * buffers, communicators); NULL is a no-op. */
 void gtcp_destroy(gtcp_ctx ctx);
+/* Text of the last error set on this context ("null context" for NULL);
+ * owned by the context, valid until the next call on it. */
 const char* gtcp_strerror(gtcp_ctx ctx);
+/* Sizes, ranks and state of the context into *out (host copy, no sync). */
 gtcp_status gtcp_info(gtcp_ctx ctx, gtcp_info_t* out);
 
 /* Load this rank's markers on the device (L-1..L-3 recipe, counter-based
@@ -253,7 +258,8 @@ gtcp_status gtcp_push(gtcp_ctx ctx, int stage);
 gtcp_status gtcp_shift(gtcp_ctx ctx);
 /* Force a bin (cell sort, H-4) now. */
 gtcp_status gtcp_bin(gtcp_ctx ctx);
-/* nsteps x [for stage in (1,2): charge, poisson_smooth, field, push(stage), shift].
+/* nsteps x [for stage in (1,2): charge, poisson_smooth, field, push(stage), shift]
+ * (with gtcp_set_fused(1) a stage's push also deposits the next charge).
  * Synchronises the stream once at the end and returns GTCP_ENONFINITE if a
  * push produced a non-finite state (checked without waiting after every
  * step as well, so a long call stops within about a step of the event). */
@@ -269,16 +275,24 @@ gtcp_status gtcp_step(gtcp_ctx ctx, int nsteps);
  * exact through the deposit's out-of-window path, only slower.  Synchronises. */
 gtcp_status gtcp_step_host(gtcp_ctx ctx, int64_t n, int64_t cap, double* const* attr, int nsteps, int64_t* n_out);
 
+/* Download a grid (GTCP_GRID_*): CHARGE / PHI as (planes 0..P) x mgrid
+ * doubles, GRADPHI as (planes 0..P) x mgrid x 3, MARKER as mpsi + 1 ring
+ * densities.  ECAPACITY if cap is below the size; synchronises. */
 gtcp_status gtcp_get_grid(gtcp_ctx ctx, int which, int64_t cap, double* host);
 /* Prescribe a grid (tests): CHARGE (then poisson_smooth uses it), PHI (then
  * field uses it) or GRADPHI (then push gathers it). */
 gtcp_status gtcp_set_grid(gtcp_ctx ctx, int which, int64_t n, const double* host);
 
+/* Counters of the context (global particle count, sum of w, reflections,
+ * clamps, fallback contributions, fixed-point scale...) into *out;
+ * GTCP_ENONFINITE if a push flagged a non-finite state; synchronises. */
 gtcp_status gtcp_stats(gtcp_ctx ctx, gtcp_stats_t* out);
 /* Diagnostics of the current live state against the current gather field
  * (call after gtcp_field, before the push, for the fields of this stage);
  * collective over all ranks; synchronises.  EINVAL if out is NULL. */
 gtcp_status gtcp_diag(gtcp_ctx ctx, gtcp_diag_t* out);
+/* Accumulated per-phase CUDA-event times and library-counted inter-GPU bytes
+ * since the last reset (phases timed only while gtcp_set_timing is on). */
 gtcp_status gtcp_timings(gtcp_ctx ctx, gtcp_timings_t* out);
 gtcp_status gtcp_timings_reset(gtcp_ctx ctx);
 /* Enable (1) / disable (0) per-phase CUDA-event timing (default off). */
