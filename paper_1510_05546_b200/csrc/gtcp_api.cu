@@ -14,6 +14,8 @@
 
 #include "gtcp_internal.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 using namespace gtcp;
 
 struct gtcp_ctx_s {
@@ -178,12 +180,17 @@ static void fold_pending(gtcp_ctx c) {
     c->pending.clear();
 }
 
+// NVTX ranges name every phase on the host timeline (nsys / ncu --nvtx);
+// header-only NVTX 3, a no-op unless a tool injects itself
+static const char* const kPhaseName[GTCP_NPHASE] = {"gtcp charge", "gtcp charge_red", "gtcp poisson_smooth",
+                                                   "gtcp field", "gtcp push", "gtcp shift", "gtcp bin"};
 struct PhaseTimer {
     gtcp_ctx c;
     int phase;
     cudaEvent_t a = nullptr;
     int prev_phase;
     PhaseTimer(gtcp_ctx c_, int ph) : c(c_), phase(ph) {
+        nvtxRangePushA(kPhaseName[ph]);
         prev_phase = c->cur_phase;
         c->cur_phase = ph;
         if (c->timing) {
@@ -192,6 +199,7 @@ struct PhaseTimer {
         }
     }
     ~PhaseTimer() {
+        nvtxRangePop();
         c->cur_phase = prev_phase;
         if (c->timing) {
             cudaEvent_t b = get_event(c);
